@@ -1,0 +1,293 @@
+"""Pins for the CPU oracle (oracle/): each check ties the oracle to something
+other than itself — a library routine (torch SDPA, numpy matmul / fp16
+conversion, scipy softmax), a closed form, an invariant, exact integer
+arithmetic, or a number the paper prints.  A plausible mistake in the oracle
+(dropped term, wrong sign or index, transposed operand, wrong softmax axis,
+mask off-by-one, missing scale) fails at least one of them.
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+import scipy.special
+import torch
+
+import mbci_inputs as gen
+import oracle
+from oracle import model
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _f64(inp):
+    """numpy (library) decode of the inputs, independent of the oracle decoder."""
+    return (gen.bits_to_f64_numpy(inp.A, inp.dtype), gen.bits_to_f64_numpy(inp.B, inp.dtype),
+            gen.bits_to_f64_numpy(inp.D, inp.dtype))
+
+
+def _bmat(inp, B):
+    """B as [batch, K, N] whatever the stored layout."""
+    return B if inp.b_layout == 0 else np.swapaxes(B, 1, 2)
+
+
+def _custom(dtype, A, B, D, b_layout):
+    """ChainInputs from explicit float arrays (exactly representable in dtype)."""
+    def bits(x):
+        x = np.asarray(x, dtype=np.float64)
+        if dtype == "f32":
+            return x.astype(np.float32).view(np.uint32)
+        if dtype == "f16":
+            return x.astype(np.float16).view(np.uint16)
+        return (x.astype(np.float32).view(np.uint32) >> np.uint32(16)).astype(np.uint16)
+    batch, M, K = A.shape
+    N, L = D.shape[1], D.shape[2]
+    return gen.ChainInputs(bits(A), bits(B), bits(D), None, dtype, batch, M, N, K, L, b_layout)
+
+
+# ---------------------------------------------------------------- decoders
+def test_decoders_match_numpy_all_fp16_bf16_patterns():
+    allbits = np.arange(65536, dtype=np.uint32).astype(np.uint16)
+    for dt in ("f16", "bf16"):
+        ours = oracle.decode(allbits, dt)
+        ref = gen.bits_to_f64_numpy(allbits, dt)
+        nan = np.isnan(ref)
+        assert np.array_equal(np.isnan(ours), nan)
+        assert np.array_equal(ours[~nan], ref[~nan]), dt
+    rng = np.random.default_rng(0)
+    f32 = rng.integers(0, 2**32, size=200000, dtype=np.uint64).astype(np.uint32)
+    ours = oracle.decode(f32, "f32")
+    ref = f32.view(np.float32).astype(np.float64)
+    nan = np.isnan(ref)
+    assert np.array_equal(ours[~nan], ref[~nan])
+
+
+# ---------------------------------------------------------------- GEMMs + layouts
+def test_hand_case():
+    # A=[[1,2]], B=[[3],[4]], D=[[5]]  =>  C = 1*3+2*4 = 11,  E = 55
+    inp = _custom("f32", np.array([[[1.0, 2.0]]]), np.array([[[3.0], [4.0]]]),
+                  np.array([[[5.0]]]), 0)
+    assert oracle.chain(inp, "none")[0, 0, 0] == 55.0
+
+
+@pytest.mark.parametrize("b_layout", [0, 1])
+@pytest.mark.parametrize("dtype", ["f32", "f16", "bf16"])
+def test_brute_force_tiny_shapes_integer_exact(dtype, b_layout):
+    """All (M,N,K,L) in {1,2,3}^4: E == A@(B@D) (associativity, numpy) exactly; SCALE by 0.5."""
+    seed = 11
+    for M in (1, 2, 3):
+        for N in (1, 2, 3):
+            for K in (1, 2, 3):
+                for L in (1, 2, 3):
+                    inp = gen.make_chain_inputs(seed, dtype, 2, M, N, K, L, b_layout, kind="int")
+                    A, B, D = _f64(inp)
+                    ref = A @ (_bmat(inp, B) @ D)
+                    assert np.array_equal(oracle.chain(inp, "none"), ref), (M, N, K, L)
+                    assert np.array_equal(oracle.chain(inp, "scale", 0.5), 0.5 * ref)
+                    seed += 1
+
+
+@pytest.mark.parametrize("b_layout", [0, 1])
+def test_integer_chain_exact_at_medium_size(b_layout):
+    inp = gen.make_chain_inputs(3, "bf16", 3, 37, 53, 16, 24, b_layout, kind="int")
+    A, B, D = _f64(inp)
+    assert np.array_equal(oracle.chain(inp, "none"), A @ (_bmat(inp, B) @ D))
+
+
+def test_layouts_agree():
+    """b_layout 1 with B stored transposed gives the same E as b_layout 0."""
+    i0 = gen.make_chain_inputs(5, "f16", 2, 9, 13, 7, 5, 0)
+    i1 = gen.ChainInputs(i0.A, np.ascontiguousarray(np.swapaxes(i0.B, 1, 2)), i0.D, None,
+                         "f16", 2, 9, 13, 7, 5, 1)
+    for op in ("none", "scale", "softmax"):
+        assert np.array_equal(oracle.chain(i0, op, 0.3), oracle.chain(i1, op, 0.3))
+
+
+# ---------------------------------------------------------------- softmax op
+@pytest.mark.parametrize("dtype,K", [("f16", 64), ("bf16", 32), ("f32", 16)])
+def test_softmax_matches_torch_sdpa(dtype, K):
+    """K = L, SOFTMAX, s = 1/sqrt(K), no mask  ==  textbook scaled dot-product attention."""
+    inp = gen.make_chain_inputs(21, dtype, 3, 40, 70, K, K, 1)
+    A, B, D = _f64(inp)
+    ours = oracle.chain(inp, "softmax", 1.0 / math.sqrt(K))
+    ref = torch.nn.functional.scaled_dot_product_attention(
+        torch.from_numpy(A), torch.from_numpy(B), torch.from_numpy(D)).numpy()
+    assert np.max(np.abs(ours - ref)) < 1e-12
+
+
+def test_softmax_key_padding_matches_torch_sdpa():
+    inp = gen.make_chain_inputs(22, "f16", 4, 33, 90, 64, 48, 1)
+    vl = np.array([90, 1, 45, 77], dtype=np.int32)
+    A, B, D = _f64(inp)
+    ours = oracle.chain(inp, "softmax", 0.125, valid_len=vl)
+    mask = torch.arange(90)[None, None, :] < torch.from_numpy(vl)[:, None, None]
+    ref = torch.nn.functional.scaled_dot_product_attention(
+        torch.from_numpy(A), torch.from_numpy(B), torch.from_numpy(D),
+        attn_mask=mask.expand(4, 33, 90), scale=0.125).numpy()
+    assert np.max(np.abs(ours - ref)) < 1e-12
+
+
+@pytest.mark.parametrize("b_layout", [0, 1])
+def test_identity_D_exposes_op(b_layout):
+    """D = I (L = N)  =>  E = op(A·B): numpy matmul and scipy softmax as references."""
+    inp = gen.make_chain_inputs(31, "bf16", 2, 17, 24, 20, 24, b_layout)
+    eye = np.broadcast_to(np.eye(24), (2, 24, 24))
+    inp = _custom("bf16", gen.bits_to_f64_numpy(inp.A, "bf16"), gen.bits_to_f64_numpy(inp.B, "bf16"),
+                  eye, b_layout)
+    A, B, _ = _f64(inp)
+    C = A @ _bmat(inp, B)
+    assert np.array_equal(oracle.chain(inp, "none"), C)
+    assert np.array_equal(oracle.chain(inp, "scale", 0.25), 0.25 * C)
+    sm = scipy.special.softmax(0.7 * C, axis=-1)
+    assert np.max(np.abs(oracle.chain(inp, "softmax", 0.7) - sm)) < 1e-13
+
+
+def test_zero_K_closed_forms():
+    inp = gen.make_chain_inputs(41, "f16", 3, 5, 11, 0, 6, 1)
+    assert np.array_equal(oracle.chain(inp, "none"), np.zeros((3, 5, 6)))
+    assert np.array_equal(oracle.chain(inp, "scale", 2.0), np.zeros((3, 5, 6)))
+    vl = np.array([11, 4, 1], dtype=np.int32)
+    D = gen.bits_to_f64_numpy(inp.D, "f16")
+    E = oracle.chain(inp, "softmax", 0.125, valid_len=vl)
+    for b in range(3):
+        ref = D[b, :vl[b]].mean(axis=0)
+        assert np.max(np.abs(E[b] - ref[None, :])) < 1e-14
+
+
+def test_scale_zero_is_uniform_mean():
+    inp = gen.make_chain_inputs(42, "bf16", 2, 9, 19, 64, 8, 0)
+    D = gen.bits_to_f64_numpy(inp.D, "bf16")
+    E = oracle.chain(inp, "softmax", 0.0)
+    assert np.max(np.abs(E - D.mean(axis=1)[:, None, :])) < 1e-14
+
+
+def test_single_and_zero_valid_key():
+    inp = gen.make_chain_inputs(43, "f16", 2, 7, 30, 64, 16, 1, sigmas=(3.0, 3.0, 1.0))
+    D = gen.bits_to_f64_numpy(inp.D, "f16")
+    E = oracle.chain(inp, "softmax", 0.125, valid_len=np.array([1, 0], dtype=np.int32))
+    assert np.array_equal(E[0], np.broadcast_to(D[0, 0], (7, 16)))   # exactly D[0,:]
+    assert np.array_equal(E[1], np.zeros((7, 16)))                    # fully masked -> 0
+
+
+def test_softmax_rows_sum_to_one_and_ones_D():
+    inp = gen.make_chain_inputs(44, "f16", 2, 12, 57, 64, 8, 1, sigmas=(3.0, 3.0, 1.0))
+    vl = np.array([57, 20], dtype=np.int32)
+    _, Cp = oracle.chain(inp, "softmax", 0.125, valid_len=vl, want_cprime=True)
+    assert np.max(np.abs(Cp.sum(axis=1) - 1.0)) <= 1e-12
+    assert np.all(Cp.reshape(2, 12, 57)[1, :, 20:] == 0.0)           # masked keys get 0
+    ones = _custom("f16", gen.bits_to_f64_numpy(inp.A, "f16"), gen.bits_to_f64_numpy(inp.B, "f16"),
+                   np.ones((2, 57, 8)), 1)
+    assert np.max(np.abs(oracle.chain(ones, "softmax", 0.125, valid_len=vl) - 1.0)) <= 1e-12
+
+
+def test_softmax_shift_invariance():
+    """Append a K-column A[:,K]=1, B[K,:]=c: every score shifts by c*s; E is unchanged."""
+    inp = gen.make_chain_inputs(45, "f32", 2, 10, 25, 16, 12, 0)
+    A, B, D = _f64(inp)
+    c = 3.0
+    A2 = np.concatenate([A, np.ones((2, 10, 1))], axis=2)
+    B2 = np.concatenate([B, np.full((2, 1, 25), c)], axis=1)
+    inp2 = _custom("f32", A2, B2, D, 0)
+    e1, e2 = oracle.chain(inp, "softmax", 0.25), oracle.chain(inp2, "softmax", 0.25)
+    assert np.max(np.abs(e1 - e2)) < 1e-13
+    # and the shift is NOT invisible to the un-normalised ops (sanity: the column is used)
+    assert not np.allclose(oracle.chain(inp, "none"), oracle.chain(inp2, "none"))
+
+
+def test_selected_rows_equal_full():
+    inp = gen.make_chain_inputs(46, "bf16", 3, 20, 33, 48, 24, 1)
+    vl = np.array([33, 10, 2], dtype=np.int32)
+    full = oracle.chain(inp, "softmax", 0.2, valid_len=vl)
+    rows = np.array([[0, 0], [2, 19], [1, 7], [2, 3]], dtype=np.int64)
+    part = oracle.chain(inp, "softmax", 0.2, valid_len=vl, rows=rows)
+    for i, (b, m) in enumerate(rows):
+        assert np.array_equal(part[i], full[b, m])
+
+
+def test_row_max_error_metric():
+    ref = np.array([[[1.0, -2.0], [0.0, 0.0]]])
+    got = np.array([[[1.0, -2.1], [0.0, 0.5]]])
+    # row 0: 0.1/2 = 0.05; row 1: all-zero reference -> absolute 0.5
+    assert oracle.row_max_error(got, ref) == pytest.approx(0.5)
+    assert oracle.row_max_error(got[:, :1], ref[:, :1]) == pytest.approx(0.05)
+    assert math.isnan(oracle.row_max_error(np.full_like(ref, np.nan), ref))
+
+
+# ---------------------------------------------------------------- paper numbers
+def _read_golden(name):
+    rows = []
+    for line in open(os.path.join(GOLDEN, name)):
+        line = line.split("#", 1)[0].strip()
+        if line:
+            rows.append(line)
+    return rows
+
+
+def test_phi_goldens():
+    for line in _read_golden("phi.txt"):
+        f, TM, TN, K, exp, tol = line.split()
+        got = getattr(model, f)(float(TM), float(TN), float(K))
+        assert abs(got - float(exp)) <= float(tol), line
+    # the two readings round to the paper's "227 to 2" only for phi_text
+    assert round(model.phi_text(256, 256, 1024)) == 228 and int(model.phi_text(256, 256, 1024)) == 227
+    assert round(model.phi_text(256, 256, 1)) == 2
+    assert round(model.phi_printed(256, 256, 1)) == 1
+
+
+def test_fused_intensity_independent_of_K_L():
+    for K, L in ((16, 16), (64, 64), (128, 32)):
+        assert model.fused_intensity(512, 512, K, L, 2) == pytest.approx(256.0)
+    assert model.fused_intensity(256, 256, 64, 64, 2) == pytest.approx(128.0)
+    assert model.fused_intensity(1024, 256, 64, 80, 2) == pytest.approx(2 * 1024 * 256 / (1280 * 2))
+
+
+def test_model_goldens():
+    g = {}
+    for line in _read_golden("model.txt"):
+        lhs, rhs = line.split("=")
+        g[lhs.strip()] = float(rhs)
+    assert len(model.deep_expressions()) == g["deep_count"]
+    assert len(set(model.deep_expressions())) == 24
+    assert len(model.flat_expressions()) == g["flat_count"]
+    assert model.space_size(1024, 1024, 512, 512) == g["space_size 1024 1024 512 512"]
+    assert model.space_size(64, 64, 32, 32) == g["space_size 64 64 32 32"]
+    assert model.alpha(108, 108) == g["alpha 108 108"]
+    assert model.alpha(1, 108) == g["alpha 1 108"]
+    assert model.alpha(10**6, 108) == pytest.approx(g["alpha 1000000 108"], abs=1e-12)
+    assert model.t_mem([(64 * 64 * 2, [4, 2])], 1e9) == pytest.approx(g["t_mem_single_load"], rel=1e-12)
+    assert model.t_comp([(2 * 64**3, [4, 4, 2])], 1e12) == pytest.approx(g["t_comp_single_compute"], rel=1e-12)
+    assert model.shm_estm([(64, 64)] * 5) * 2 == g["shm_estm_five_64x64_fp16"]
+    assert not model.rule4_reject(40960, 48 * 1024)
+    assert model.rule4_reject(100000, 65536)
+    assert model.t_estm(6.5536e-5, 1.6777216e-5, 2.0) == pytest.approx(2 * (6.5536e-5 + 1.6777216e-5))
+
+
+def test_rule3_and_tile_options():
+    assert model.rule3_reject(1024, 48)          # power of 2, padded
+    assert not model.rule3_reject(1000, 48)      # 8/1000 < 0.05
+    assert not model.rule3_reject(1024, 64)
+    assert model.rule3_reject(100, 48)           # 44/100 >= 0.05
+    assert model.tile_options(40) == [16, 32, 48]
+    assert model.tile_options(16) == [16]
+
+
+def test_chain_schedule_dead_loop_and_hoist():
+    """with k dead, L_A executes l_m times instead of l_m*l_h*l_n*l_k;
+    PAPER.md:232: S_E is hoisted out of n (trip l_m*l_h)."""
+    mem, comp, nb = model.chain_schedule(1, 512, 512, 64, 64, 128, 128, 64, 64, 2)
+    la, lb, ld, se = mem
+    assert math.prod(la[1]) == 4            # l_m, dead k
+    assert math.prod(lb[1]) == 4 * 1 * 4 * 1
+    assert math.prod(se[1]) == 4            # not multiplied by l_n = 4
+    mem2, _, _ = model.chain_schedule(1, 512, 512, 128, 64, 128, 128, 64, 64, 2)
+    assert math.prod(mem2[0][1]) == 4 * 1 * 4 * 2   # live k: L_A under m,h,n,k
+    # total FLOPs do not depend on TM/TN: 2MN(K+L) per batch when h is dead ...
+    for TN in (64, 128, 256):
+        _, comp, _ = model.chain_schedule(2, 512, 512, 64, 64, 128, TN, 64, 64, 2)
+        assert sum(fp * math.prod(lp) for fp, lp in comp) == 2 * 2 * 512 * 512 * 128
+    # ... while chunking L onto the grid (l_h = 2) recomputes C_C l_h times
+    _, comp, _ = model.chain_schedule(2, 512, 512, 64, 64, 128, 128, 64, 32, 2)
+    assert sum(fp * math.prod(lp) for fp, lp in comp) == 2 * 2 * 512 * 512 * (2 * 64 + 64)
+    # hoisted bytes equal the algorithmic (M+N)(K+L)s per batch when every tile covers its dim
+    mem, _, _ = model.chain_schedule(1, 256, 256, 64, 64, 256, 256, 64, 64, 2)
+    assert sum(ts * math.prod(lp) for ts, lp in mem) == (256 + 256) * (64 + 64) * 2
