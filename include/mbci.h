@@ -1,0 +1,174 @@
+/*
+ * mbci.h — C ABI of the B200-native fused MBCI chain  E = op(A·B)·D.
+ *
+ * The operation (MCFuser, arXiv 2506.22169; citations are PAPER.md line numbers):
+ *   PAPER.md:196 (§III-A, Fig. 3)  "the GEMM chain (C = A×B, E = C×D)" with cross-tile
+ *                                  loops m, n, k, h;
+ *   PAPER.md:489 (§VI-B1)          batched layouts "(batch, M, K) × (batch, K, N)" then
+ *                                  "(batch, M, N) × (batch, N, H)";  this ABI writes L for H;
+ *   PAPER.md:498 (§VI-B2)          self-attention: a softmax between the two contractions;
+ *   PAPER.md:253 (§III-B)          with K <= 128 the k loop is dead, A is loaded once per
+ *                                  CTA and C never leaves the chip (one fused kernel).
+ * For every batch index b (b = batch x heads):
+ *   C[m,n] = sum_k A[b,m,k] * B[b,k,n]                  (fp32 accumulate)
+ *   NONE:    C' = C
+ *   SCALE:   C' = scale * C
+ *   SOFTMAX: C'[m,:] = softmax_n(scale * C[m,:] + mask), mask = -inf for keys
+ *            n >= valid_len[b] (KEY_PADDING); a row with no valid key gives E = 0
+ *   E[b,m,l] = sum_n C'[m,n] * D[b,n,l]                 (fp32 accumulate, stored as dtype)
+ * The readings behind scale / mask / softmax axis are DESIGN.md §2 R1-R4.
+ *
+ * Conventions: all sizes and strides are int64 ELEMENT counts; pointers are
+ * plain host or device pointers as stated per call; no C++ exception crosses
+ * the ABI; every call returns an mbci_status_t; a thread-local detail string is
+ * available from mbci_last_error().
+ */
+#ifndef MBCI_H_
+#define MBCI_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MBCI_ABI_VERSION 1
+
+typedef struct mbci_chain* mbci_chain_t;   /* opaque; created/owned by the library */
+
+typedef enum { MBCI_F32 = 0, MBCI_F16 = 1, MBCI_BF16 = 2 } mbci_dtype_t;
+typedef enum { MBCI_OP_NONE = 0, MBCI_OP_SCALE = 1, MBCI_OP_SOFTMAX = 2 } mbci_op_t;
+typedef enum { MBCI_MASK_NONE = 0, MBCI_MASK_KEY_PADDING = 1 } mbci_mask_t;
+typedef enum {
+  MBCI_OK = 0,
+  MBCI_ERR_INVALID = 1,      /* user error: NULL pointer, negative dim, bad enum, missing valid_len */
+  MBCI_ERR_UNSUPPORTED = 2,  /* legal but outside this build: K or L > 128, misaligned TMA strides
+                                with no fallback, no sm_100 device */
+  MBCI_ERR_CUDA = 3,         /* CUDA runtime / driver failure (detail in mbci_last_error) */
+  MBCI_ERR_NOMEM = 4         /* host or device allocation failed */
+} mbci_status_t;
+
+/* Problem descriptor.  A, B, D, E share `dtype`; accumulation is fp32.
+ * Layouts (row-major inside each batch slice, strides in elements):
+ *   A  [batch, M, K]  element (b,m,k) at  b*bs_a + m*ld_a + k
+ *   B  b_layout 0: [batch, K, N]  (b,k,n) at b*bs_b + k*ld_b + n
+ *      b_layout 1: [batch, N, K]  (b,n,k) at b*bs_b + n*ld_b + k   (attention's K matrix)
+ *   D  [batch, N, L]  (b,n,l) at  b*bs_d + n*ld_d + l
+ *   E  [batch, M, L]  (b,m,l) at  b*bs_e + m*ld_e + l
+ * A stride of 0 means "packed" (ld = inner extent, bs = rows*ld). */
+typedef struct {
+  int64_t batch, M, N, K, L;
+  int32_t dtype;        /* mbci_dtype_t */
+  int32_t op;           /* mbci_op_t */
+  float scale;          /* SCALE / SOFTMAX multiplier; NaN selects 1/sqrt(K) (DESIGN R1) */
+  int32_t mask;         /* mbci_mask_t; KEY_PADDING only with SOFTMAX */
+  int32_t b_layout;     /* 0 or 1, see above */
+  int64_t ld_a, ld_b, ld_d, ld_e;
+  int64_t bs_a, bs_b, bs_d, bs_e;
+  int32_t tune;         /* 0: analytical model picks the plan; 1: also time the top-8 at create */
+} mbci_chain_desc_t;
+
+/* Hardware description used by the tile selector (Eqs. 2-5). */
+typedef struct {
+  double W;             /* HBM bandwidth, bytes/s */
+  double P;             /* dense 16-bit tensor throughput, FLOP/s */
+  int32_t n_sm;         /* streaming multiprocessors */
+  int32_t smem_max;     /* max dynamic shared memory per CTA, bytes */
+  int32_t tmem_cols;    /* tensor-memory columns per SM (512 on sm_100) */
+  double sfu_per_clk_sm;/* ex2 results per clock per SM (16 on sm_100) */
+  double clock_hz;      /* SM clock used for the SFU term */
+} mbci_hw_t;
+
+/* One candidate plan: the paper's tile sizes (T_M, T_N, T_K, T_H) for the
+ * flat expression mh(n(k(L_A,L_B,C_C),L_D,C_E),S_E), plus B200 pipeline parameters and the
+ * model terms of Eqs. (2)-(5).  kernel: 0 = tcgen05 fused chain, 1 = SIMT (CUDA cores). */
+typedef struct {
+  int32_t kernel;
+  int32_t BM, BN, TK, TL;   /* T_M, T_N, T_K (= padded K: dead k loop), T_H */
+  int32_t stages;           /* B/D shared-memory ring depth */
+  int32_t smem_bytes, tmem_cols;
+  int64_t n_block;          /* CTAs = batch * l_m * l_h */
+  double t_mem, t_comp, alpha, t_estm;   /* PAPER.md Eqs. (3), (4), (5), (2), seconds */
+  double t_b200;            /* B200 extension: max(HBM, tensor, SFU) x wave quantisation */
+} mbci_plan_t;
+
+/* ---- lifecycle -------------------------------------------------------------------------- */
+
+/* Validate `desc`, pick a plan (tile selector) for `device`, and return a handle.
+ * Host-only unless desc->tune == 1 (then it allocates scratch and times candidates on
+ * `device`).  Errors: INVALID (NULL, negative dims, bad enums), UNSUPPORTED (K or L > 128,
+ * device is not sm_100), CUDA, NOMEM. */
+mbci_status_t mbci_chain_create(const mbci_chain_desc_t* desc, int device, mbci_chain_t* out);
+
+/* As mbci_chain_create with an explicit plan (tests: plan invariance).  Fields used: kernel,
+ * BN, TL, stages; the rest is recomputed.  UNSUPPORTED if the plan is illegal for desc. */
+mbci_status_t mbci_chain_create_with_plan(const mbci_chain_desc_t* desc, int device,
+                                          const mbci_plan_t* plan, mbci_chain_t* out);
+
+/* Enqueue one evaluation of the chain on `stream` (cudaStream_t; NULL = legacy default).
+ * A, B, D, E are DEVICE pointers on the handle's device with the descriptor's layout, each
+ * 16-byte aligned for the tcgen05 path; E must not alias A, B or D.  valid_len is a DEVICE
+ * int32[batch] (required iff mask == KEY_PADDING; values clamp to [0, N]).
+ * Asynchronous: no allocation, no host synchronisation.  Degenerate shapes: batch, M or
+ * L == 0 launch nothing; N == 0 (or every key masked) writes E = 0; K == 0 treats C as 0.
+ * Errors: INVALID (NULL handle/pointers), UNSUPPORTED (misaligned pointer on the tensor-core
+ * path), CUDA (launch failure). */
+mbci_status_t mbci_chain_run(mbci_chain_t h, const void* A, const void* B, const void* D,
+                             void* E, const int32_t* valid_len, void* stream);
+
+/* End-to-end convenience: A, B, D, E and valid_len are HOST pointers (pinned memory gives
+ * asynchronous copies).  Copies the inputs to handle-owned device buffers (allocated on
+ * first use and kept), runs the chain, copies E back, and synchronises `stream` before
+ * returning.  Same layouts, strides and errors as mbci_chain_run, plus NOMEM. */
+mbci_status_t mbci_chain_run_host(mbci_chain_t h, const void* A, const void* B, const void* D,
+                                  void* E, const int32_t* valid_len, void* stream);
+
+/* Free the handle and its device scratch.  The caller must have synchronised every stream
+ * the handle ran on.  NULL is a no-op. */
+mbci_status_t mbci_chain_destroy(mbci_chain_t h);
+
+/* ---- introspection ---------------------------------------------------------------------- */
+
+/* The chosen plan (copy). */
+mbci_status_t mbci_chain_plan(mbci_chain_t h, mbci_plan_t* out);
+
+/* Human-readable plan description into buf (NUL-terminated, truncated to len). */
+mbci_status_t mbci_chain_describe(mbci_chain_t h, char* buf, size_t len);
+
+/* Number of kernel launches one mbci_chain_run performs for this handle (0 or 1). */
+int32_t mbci_chain_launches_per_run(mbci_chain_t h);
+
+const char* mbci_status_string(mbci_status_t s);
+const char* mbci_last_error(void);   /* thread-local; valid until the next call on this thread */
+int32_t mbci_abi_version(void);
+
+/* ---- tile selector (host only; never touches a GPU) ------------------------------------- */
+
+/* Default B200 hardware description: W and P from MEASURED_PEAKS-style figures, 148 SMs,
+ * 232448 B shared memory, 512 TMEM columns, 16 ex2/clk/SM at 1.965 GHz. */
+void mbci_hw_default(mbci_hw_t* hw);
+
+/* Enumerate the legal candidate plans for desc on hw (after Rule 3, and the
+ * exact SMEM / TMEM budgets that replace Rule 4's estimate), each with its
+ * model terms.  Writes at most cap plans; *n_out receives the total count.  INVALID on
+ * bad desc; UNSUPPORTED if no plan is legal. */
+mbci_status_t mbci_plan_enumerate(const mbci_chain_desc_t* desc, const mbci_hw_t* hw,
+                                  mbci_plan_t* plans, int32_t cap, int32_t* n_out);
+
+/* The plan the selector picks without measurement (smallest t_b200; ties -> t_estm). */
+mbci_status_t mbci_plan_select(const mbci_chain_desc_t* desc, const mbci_hw_t* hw,
+                               mbci_plan_t* out);
+
+/* Paper model terms (Eqs. 2-5) for an arbitrary tile vector of the flat chain schedule
+ * mh(n(k(L_A,L_B,C_C),L_D,C_E),S_E) with dead-loop elimination.
+ * elem_bytes = s.  Writes {t_mem, t_comp, alpha, t_estm} into out[0..3] and N_block to
+ * out[4]. */
+mbci_status_t mbci_model_terms(int64_t batch, int64_t M, int64_t N, int64_t K, int64_t L,
+                               int64_t TM, int64_t TN, int64_t TK, int64_t TH, int32_t elem_bytes,
+                               const mbci_hw_t* hw, double out[5]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MBCI_H_ */

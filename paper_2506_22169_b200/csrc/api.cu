@@ -1,0 +1,592 @@
+// api.cu — the C ABI (include/mbci.h): validation, plan selection, TMA descriptor encoding,
+// launches, end-to-end host entry, and the selector's host-only entry points.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/mbci.h"
+#include "chain_simt.cuh"
+#include "chain_tc.cuh"
+#include "selector.h"
+
+using namespace mbci;
+
+namespace {
+
+thread_local std::string g_err;
+
+mbci_status_t fail(mbci_status_t s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+mbci_status_t cuda_fail(cudaError_t e, const char* what) {
+  return fail(MBCI_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+// Validate and fill packed strides.
+mbci_status_t normalize(const mbci_chain_desc_t* in, mbci_chain_desc_t* d) {
+  if (!in) return fail(MBCI_ERR_INVALID, "desc is NULL");
+  *d = *in;
+  if (d->batch < 0 || d->M < 0 || d->N < 0 || d->K < 0 || d->L < 0)
+    return fail(MBCI_ERR_INVALID, "negative dimension");
+  if (d->dtype < MBCI_F32 || d->dtype > MBCI_BF16) return fail(MBCI_ERR_INVALID, "bad dtype %d", d->dtype);
+  if (d->op < MBCI_OP_NONE || d->op > MBCI_OP_SOFTMAX) return fail(MBCI_ERR_INVALID, "bad op %d", d->op);
+  if (d->mask != MBCI_MASK_NONE && d->mask != MBCI_MASK_KEY_PADDING)
+    return fail(MBCI_ERR_INVALID, "bad mask %d", d->mask);
+  if (d->mask == MBCI_MASK_KEY_PADDING && d->op != MBCI_OP_SOFTMAX)
+    return fail(MBCI_ERR_INVALID, "KEY_PADDING requires op SOFTMAX");
+  if (d->b_layout != 0 && d->b_layout != 1) return fail(MBCI_ERR_INVALID, "bad b_layout %d", d->b_layout);
+  if (d->tune != 0 && d->tune != 1) return fail(MBCI_ERR_INVALID, "bad tune %d", d->tune);
+  if (d->K > 128 || d->L > 128)
+    return fail(MBCI_ERR_UNSUPPORTED, "K=%lld L=%lld: this build fuses K, L <= 128 only",
+                (long long)d->K, (long long)d->L);
+  const int64_t b_inner = d->b_layout == 0 ? d->N : d->K;
+  const int64_t b_rows = d->b_layout == 0 ? d->K : d->N;
+  if (d->ld_a == 0) d->ld_a = d->K;
+  if (d->ld_b == 0) d->ld_b = b_inner;
+  if (d->ld_d == 0) d->ld_d = d->L;
+  if (d->ld_e == 0) d->ld_e = d->L;
+  if (d->bs_a == 0) d->bs_a = d->M * d->ld_a;
+  if (d->bs_b == 0) d->bs_b = b_rows * d->ld_b;
+  if (d->bs_d == 0) d->bs_d = d->N * d->ld_d;
+  if (d->bs_e == 0) d->bs_e = d->M * d->ld_e;
+  if (d->ld_a < d->K || d->ld_b < b_inner || d->ld_d < d->L || d->ld_e < d->L)
+    return fail(MBCI_ERR_INVALID, "row stride smaller than the row");
+  if (d->ld_a < 0 || d->ld_b < 0 || d->ld_d < 0 || d->ld_e < 0 || d->bs_a < 0 || d->bs_b < 0 ||
+      d->bs_d < 0 || d->bs_e < 0)
+    return fail(MBCI_ERR_INVALID, "negative stride");
+  if (d->M > INT32_MAX || d->N > INT32_MAX || d->batch > INT32_MAX)
+    return fail(MBCI_ERR_UNSUPPORTED, "dimension exceeds int32");
+  if (std::isnan(d->scale)) d->scale = d->K > 0 ? 1.0f / std::sqrt(static_cast<float>(d->K)) : 1.0f;
+  return MBCI_OK;
+}
+
+int64_t span_elems(int64_t batch, int64_t rows, int64_t cols, int64_t ld, int64_t bs) {
+  if (batch == 0 || rows == 0 || cols == 0) return 0;
+  return (batch - 1) * bs + (rows - 1) * ld + cols;
+}
+
+using TcKernel = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, TcParams);
+
+template <bool BF16, int BN, int KCH, int BL>
+TcKernel pick_d(int dch) {
+  return dch == 1 ? (TcKernel)k_chain_tc<BF16, BN, KCH, BL, 1> : (TcKernel)k_chain_tc<BF16, BN, KCH, BL, 2>;
+}
+template <bool BF16, int BN, int KCH>
+TcKernel pick_bl(int bl, int dch) {
+  return bl == 0 ? pick_d<BF16, BN, KCH, 0>(dch) : pick_d<BF16, BN, KCH, 1>(dch);
+}
+template <bool BF16, int BN>
+TcKernel pick_kch(int kch, int bl, int dch) {
+  return kch == 1 ? pick_bl<BF16, BN, 1>(bl, dch) : pick_bl<BF16, BN, 2>(bl, dch);
+}
+template <bool BF16>
+TcKernel pick_bn(int bn, int kch, int bl, int dch) {
+  return bn == 64 ? pick_kch<BF16, 64>(kch, bl, dch) : pick_kch<BF16, 128>(kch, bl, dch);
+}
+TcKernel pick_tc(bool bf16, int bn, int kch, int bl, int dch) {
+  return bf16 ? pick_bn<true>(bn, kch, bl, dch) : pick_bn<false>(bn, kch, bl, dch);
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+std::once_flag g_encode_once;
+
+mbci_status_t get_encoder() {
+  std::call_once(g_encode_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  if (!g_encode) return fail(MBCI_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  return MBCI_OK;
+}
+
+// 3-D tiled map over [batch][rows][cols] (cols contiguous), box {64, box_rows, 1}, 128-B swizzle.
+mbci_status_t encode3d(CUtensorMap* map, const void* base, bool bf16, int64_t cols, int64_t rows,
+                       int64_t batch, int64_t ld, int64_t bs, uint32_t box_rows) {
+  memset(map, 0, sizeof(*map));
+  cuuint64_t dims[3] = {(cuuint64_t)std::max<int64_t>(cols, 1), (cuuint64_t)std::max<int64_t>(rows, 1),
+                        (cuuint64_t)std::max<int64_t>(batch, 1)};
+  cuuint64_t strides[2] = {(cuuint64_t)(std::max<int64_t>(ld, 8) * 2),
+                           (cuuint64_t)(std::max<int64_t>(bs, 8) * 2)};
+  cuuint32_t box[3] = {64, box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = g_encode(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3,
+                        const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(MBCI_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d): cols=%lld rows=%lld ld=%lld bs=%lld",
+                (int)r, (long long)cols, (long long)rows, (long long)ld, (long long)bs);
+  return MBCI_OK;
+}
+
+struct MapCacheEntry {
+  const void *A = nullptr, *B = nullptr, *D = nullptr;
+  CUtensorMap ta, tb, td;
+  uint64_t stamp = 0;
+};
+
+}  // namespace
+
+struct mbci_chain {
+  mbci_chain_desc_t d{};
+  mbci_plan_t plan{};
+  int device = 0;
+  // tensor-core path
+  TcKernel tc = nullptr;
+  TcParams tp{};
+  int32_t kch = 1, dch = 1;
+  MapCacheEntry cache[8];
+  uint64_t stamp = 0;
+  // end-to-end scratch
+  void *dA = nullptr, *dB = nullptr, *dD = nullptr, *dE = nullptr;
+  int32_t* dV = nullptr;
+  size_t nA = 0, nB = 0, nD = 0, nE = 0;
+};
+
+namespace {
+
+int32_t elem_size(const mbci_chain_desc_t& d) { return d.dtype == MBCI_F32 ? 4 : 2; }
+
+mbci_status_t setup_plan(mbci_chain* h) {
+  const mbci_chain_desc_t& d = h->d;
+  mbci_plan_t& p = h->plan;
+  if (p.kernel == 0) {
+    const int32_t k_steps = static_cast<int32_t>((d.K + 15) / 16);
+    int32_t a_bytes, b_stage, d_stage;
+    p.smem_bytes = static_cast<int32_t>(
+        tc_smem_bytes(k_steps, p.BN, p.TL, p.stages, d.b_layout, &a_bytes, &b_stage, &d_stage));
+    p.tmem_cols = tmem_alloc_cols(p.BN, p.TL);
+    h->kch = std::max(1, (16 * k_steps + 63) / 64);
+    h->dch = (p.TL + 63) / 64;
+    h->tc = pick_tc(d.dtype == MBCI_BF16, p.BN, h->kch, d.b_layout, h->dch);
+    TcParams& t = h->tp;
+    t.M = (int32_t)d.M;
+    t.N = (int32_t)d.N;
+    t.K = (int32_t)d.K;
+    t.L = (int32_t)d.L;
+    t.batch = (int32_t)d.batch;
+    t.l_m = (int32_t)((d.M + 127) / 128);
+    t.l_h = (int32_t)((d.L + p.TL - 1) / p.TL);
+    t.TL = p.TL;
+    t.k_steps = k_steps;
+    t.stages = p.stages;
+    t.op = d.op;
+    t.scale = d.op == MBCI_OP_SOFTMAX ? d.scale * 1.4426950408889634f : d.scale;
+    t.ld_e = d.ld_e;
+    t.bs_e = d.bs_e;
+    t.a_bytes = (uint32_t)a_bytes;
+    t.b_stage_bytes = (uint32_t)b_stage;
+    t.d_stage_bytes = (uint32_t)d_stage;
+    t.kp_rows = (uint32_t)(16 * k_steps);
+    t.tmem_cols = (uint32_t)p.tmem_cols;
+    const uint32_t fmt = d.dtype == MBCI_BF16 ? 1u : 0u;
+    t.idesc1 = ptx::idesc_f16(fmt, 0, d.b_layout == 0 ? 1u : 0u, 128, (uint32_t)p.BN);
+    t.idesc2 = ptx::idesc_f16(fmt, 0, 1u, 128, (uint32_t)p.TL);
+    p.n_block = (int64_t)d.batch * t.l_m * t.l_h;
+    cudaError_t e = cudaFuncSetAttribute((const void*)h->tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         p.smem_bytes);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+  } else {
+    p.n_block = d.batch * d.M;
+    const void* fn = d.dtype == MBCI_F32 ? (const void*)k_chain_simt<float>
+                     : d.dtype == MBCI_F16 ? (const void*)k_chain_simt<__half>
+                                           : (const void*)k_chain_simt<__nv_bfloat16>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_bytes);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+  }
+  return MBCI_OK;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+mbci_status_t launch(mbci_chain* h, const void* A, const void* B, const void* D, void* E,
+                     const int32_t* valid_len, cudaStream_t st) {
+  const mbci_chain_desc_t& d = h->d;
+  if (d.batch == 0 || d.M == 0 || d.L == 0) return MBCI_OK;  // nothing to write
+  if (!E) return fail(MBCI_ERR_INVALID, "E is NULL");
+  if (d.N > 0 && d.L > 0 && !D) return fail(MBCI_ERR_INVALID, "D is NULL");
+  if (d.K > 0 && d.N > 0 && (!A || !B)) return fail(MBCI_ERR_INVALID, "A or B is NULL");
+  if (d.mask == MBCI_MASK_KEY_PADDING && !valid_len)
+    return fail(MBCI_ERR_INVALID, "mask KEY_PADDING needs valid_len");
+  const int32_t* vl = d.mask == MBCI_MASK_KEY_PADDING ? valid_len : nullptr;
+  if (h->plan.kernel == 0) {
+    if (!aligned16(E) || (d.N > 0 && !aligned16(D)) || (d.K > 0 && d.N > 0 && (!aligned16(A) || !aligned16(B))))
+      return fail(MBCI_ERR_UNSUPPORTED, "tensor-core path needs 16-byte aligned A, B, D, E");
+    // tensor maps (cached by pointer triple)
+    MapCacheEntry* ent = nullptr;
+    for (auto& c : h->cache)
+      if (c.stamp && c.A == A && c.B == B && c.D == D) ent = &c;
+    if (!ent) {
+      ent = &h->cache[0];
+      for (auto& c : h->cache)
+        if (c.stamp < ent->stamp) ent = &c;
+      mbci_status_t s = get_encoder();
+      if (s != MBCI_OK) return s;
+      const bool bf16 = d.dtype == MBCI_BF16;
+      memset(&ent->ta, 0, sizeof(CUtensorMap));
+      memset(&ent->tb, 0, sizeof(CUtensorMap));
+      memset(&ent->td, 0, sizeof(CUtensorMap));
+      if (d.K > 0 && d.N > 0) {
+        s = encode3d(&ent->ta, A, bf16, d.K, d.M, d.batch, d.ld_a, d.bs_a, 128);
+        if (s != MBCI_OK) return s;
+        if (d.b_layout == 1)
+          s = encode3d(&ent->tb, B, bf16, d.K, d.N, d.batch, d.ld_b, d.bs_b, (uint32_t)h->plan.BN);
+        else
+          s = encode3d(&ent->tb, B, bf16, d.N, d.K, d.batch, d.ld_b, d.bs_b, h->tp.kp_rows);
+        if (s != MBCI_OK) return s;
+      }
+      if (d.N > 0) {
+        s = encode3d(&ent->td, D, bf16, d.L, d.N, d.batch, d.ld_d, d.bs_d, (uint32_t)h->plan.BN);
+        if (s != MBCI_OK) return s;
+      }
+      ent->A = A;
+      ent->B = B;
+      ent->D = D;
+    }
+    ent->stamp = ++h->stamp;
+    TcParams t = h->tp;
+    t.valid_len = vl;
+    t.E = E;
+    h->tc<<<(unsigned)h->plan.n_block, kThreads, h->plan.smem_bytes, st>>>(ent->ta, ent->tb, ent->td, t);
+  } else {
+    SimtParams sp{};
+    sp.M = (int32_t)d.M;
+    sp.N = (int32_t)d.N;
+    sp.K = (int32_t)d.K;
+    sp.L = (int32_t)d.L;
+    sp.op = d.op;
+    sp.scale = d.scale;
+    sp.b_layout = d.b_layout;
+    sp.valid_len = vl;
+    sp.ld_a = d.ld_a; sp.ld_b = d.ld_b; sp.ld_d = d.ld_d; sp.ld_e = d.ld_e;
+    sp.bs_a = d.bs_a; sp.bs_b = d.bs_b; sp.bs_d = d.bs_d; sp.bs_e = d.bs_e;
+    const unsigned grid = (unsigned)(d.batch * d.M);
+    const int smem = h->plan.smem_bytes;
+    if (d.dtype == MBCI_F32)
+      k_chain_simt<float><<<grid, kSimtThreads, smem, st>>>((const float*)A, (const float*)B,
+                                                             (const float*)D, (float*)E, sp);
+    else if (d.dtype == MBCI_F16)
+      k_chain_simt<__half><<<grid, kSimtThreads, smem, st>>>((const __half*)A, (const __half*)B,
+                                                              (const __half*)D, (__half*)E, sp);
+    else
+      k_chain_simt<__nv_bfloat16><<<grid, kSimtThreads, smem, st>>>(
+          (const __nv_bfloat16*)A, (const __nv_bfloat16*)B, (const __nv_bfloat16*)D, (__nv_bfloat16*)E, sp);
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+  return MBCI_OK;
+}
+
+mbci_status_t check_device(int device) {
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
+  if (device < 0 || device >= count) return fail(MBCI_ERR_INVALID, "device %d out of range (%d)", device, count);
+  cudaDeviceProp prop;
+  e = cudaGetDeviceProperties(&prop, device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceProperties");
+  if (prop.major != 10 || prop.minor != 0)
+    return fail(MBCI_ERR_UNSUPPORTED, "device %d is sm_%d%d; this build targets sm_100a", device, prop.major,
+                prop.minor);
+  return MBCI_OK;
+}
+
+mbci_status_t tune_plan(mbci_chain* h, const std::vector<mbci_plan_t>& plans) {
+  // PAPER.md Alg. 1 lines 5-9: estimate all, measure the top n = 8.
+  const mbci_chain_desc_t& d = h->d;
+  const int64_t s = elem_size(d);
+  const int64_t b_rows = d.b_layout == 0 ? d.K : d.N, b_cols = d.b_layout == 0 ? d.N : d.K;
+  const size_t nA = span_elems(d.batch, d.M, d.K, d.ld_a, d.bs_a) * s;
+  const size_t nB = span_elems(d.batch, b_rows, b_cols, d.ld_b, d.bs_b) * s;
+  const size_t nD = span_elems(d.batch, d.N, d.L, d.ld_d, d.bs_d) * s;
+  const size_t nE = span_elems(d.batch, d.M, d.L, d.ld_e, d.bs_e) * s;
+  void *A = nullptr, *B = nullptr, *D = nullptr, *E = nullptr;
+  int32_t* V = nullptr;
+  cudaStream_t st = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  mbci_status_t rc = MBCI_OK;
+  float best = 1e30f;
+  mbci_plan_t best_plan = plans[0];
+  const int n_try = std::min<int>(8, (int)plans.size());
+  if (cudaMalloc(&A, std::max<size_t>(nA, 16)) != cudaSuccess || cudaMalloc(&B, std::max<size_t>(nB, 16)) != cudaSuccess ||
+      cudaMalloc(&D, std::max<size_t>(nD, 16)) != cudaSuccess || cudaMalloc(&E, std::max<size_t>(nE, 16)) != cudaSuccess ||
+      cudaMalloc(&V, std::max<int64_t>(d.batch, 1) * 4) != cudaSuccess) {
+    rc = fail(MBCI_ERR_NOMEM, "tune scratch allocation failed");
+    goto done;
+  }
+  cudaMemset(A, 0, nA);
+  cudaMemset(B, 0, nB);
+  cudaMemset(D, 0, nD);
+  {
+    std::vector<int32_t> hv(std::max<int64_t>(d.batch, 1), (int32_t)d.N);
+    cudaMemcpy(V, hv.data(), hv.size() * 4, cudaMemcpyHostToDevice);
+  }
+  cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  for (int i = 0; i < n_try; ++i) {
+    h->plan = plans[i];
+    for (auto& c : h->cache) c = MapCacheEntry{};
+    rc = setup_plan(h);
+    if (rc != MBCI_OK) goto done;
+    for (int w = 0; w < 2; ++w) launch(h, A, B, D, E, V, st);
+    cudaEventRecord(e0, st);
+    for (int r = 0; r < 5; ++r) launch(h, A, B, D, E, V, st);
+    cudaEventRecord(e1, st);
+    cudaError_t ce = cudaEventSynchronize(e1);
+    if (ce != cudaSuccess) {
+      rc = cuda_fail(ce, "tuning run");
+      goto done;
+    }
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (ms < best) {
+      best = ms;
+      best_plan = plans[i];
+    }
+  }
+  h->plan = best_plan;
+  for (auto& c : h->cache) c = MapCacheEntry{};
+  rc = setup_plan(h);
+done:
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
+  if (st) cudaStreamDestroy(st);
+  cudaFree(A);
+  cudaFree(B);
+  cudaFree(D);
+  cudaFree(E);
+  cudaFree(V);
+  return rc;
+}
+
+mbci_status_t create_impl(const mbci_chain_desc_t* desc, int device, const mbci_plan_t* forced,
+                          mbci_chain_t* out) {
+  if (!out) return fail(MBCI_ERR_INVALID, "out is NULL");
+  *out = nullptr;
+  mbci_chain_desc_t d;
+  mbci_status_t s = normalize(desc, &d);
+  if (s != MBCI_OK) return s;
+  s = check_device(device);
+  if (s != MBCI_OK) return s;
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  mbci_hw_t hw;
+  hw_default(&hw);
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) == cudaSuccess) {
+    hw.n_sm = prop.multiProcessorCount;
+    hw.smem_max = (int32_t)prop.sharedMemPerBlockOptin;
+  }
+  std::vector<mbci_plan_t> plans;
+  enumerate_plans(d, hw, plans);
+  if (plans.empty())
+    return fail(MBCI_ERR_UNSUPPORTED, "no legal plan (N=%lld too large for the CUDA-core path?)", (long long)d.N);
+  mbci_chain* h = new (std::nothrow) mbci_chain();
+  if (!h) return fail(MBCI_ERR_NOMEM, "handle allocation failed");
+  h->d = d;
+  h->device = device;
+  h->plan = plans[0];
+  if (forced) {
+    bool found = false;
+    for (const auto& p : plans)
+      if (p.kernel == forced->kernel && (p.kernel == 1 || (p.BN == forced->BN && p.TL == forced->TL &&
+                                                           p.stages == forced->stages))) {
+        h->plan = p;
+        found = true;
+      }
+    if (!found) {
+      delete h;
+      return fail(MBCI_ERR_UNSUPPORTED, "forced plan (kernel=%d BN=%d TL=%d stages=%d) is not legal here",
+                  forced->kernel, forced->BN, forced->TL, forced->stages);
+    }
+  }
+  s = setup_plan(h);
+  if (s == MBCI_OK && !forced && d.tune == 1 && plans.size() > 1) s = tune_plan(h, plans);
+  if (s != MBCI_OK) {
+    delete h;
+    return s;
+  }
+  *out = h;
+  return MBCI_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+mbci_status_t mbci_chain_create(const mbci_chain_desc_t* desc, int device, mbci_chain_t* out) {
+  return create_impl(desc, device, nullptr, out);
+}
+
+mbci_status_t mbci_chain_create_with_plan(const mbci_chain_desc_t* desc, int device,
+                                          const mbci_plan_t* plan, mbci_chain_t* out) {
+  if (!plan) return fail(MBCI_ERR_INVALID, "plan is NULL");
+  return create_impl(desc, device, plan, out);
+}
+
+mbci_status_t mbci_chain_run(mbci_chain_t h, const void* A, const void* B, const void* D, void* E,
+                             const int32_t* valid_len, void* stream) {
+  if (!h) return fail(MBCI_ERR_INVALID, "handle is NULL");
+  return launch(h, A, B, D, E, valid_len, reinterpret_cast<cudaStream_t>(stream));
+}
+
+mbci_status_t mbci_chain_run_host(mbci_chain_t h, const void* A, const void* B, const void* D, void* E,
+                                  const int32_t* valid_len, void* stream) {
+  if (!h) return fail(MBCI_ERR_INVALID, "handle is NULL");
+  const mbci_chain_desc_t& d = h->d;
+  if (d.batch == 0 || d.M == 0 || d.L == 0) return MBCI_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t s = elem_size(d);
+  const int64_t b_rows = d.b_layout == 0 ? d.K : d.N, b_cols = d.b_layout == 0 ? d.N : d.K;
+  const size_t nA = span_elems(d.batch, d.M, d.K, d.ld_a, d.bs_a) * s;
+  const size_t nB = span_elems(d.batch, b_rows, b_cols, d.ld_b, d.bs_b) * s;
+  const size_t nD = span_elems(d.batch, d.N, d.L, d.ld_d, d.bs_d) * s;
+  const size_t nE = span_elems(d.batch, d.M, d.L, d.ld_e, d.bs_e) * s;
+  cudaError_t e = cudaSetDevice(h->device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  auto ensure = [&](void** p, size_t* have, size_t need) -> bool {
+    if (*have >= need && *p) return true;
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+    *have = 0;
+    if (cudaMalloc(p, std::max<size_t>(need, 16)) != cudaSuccess) return false;
+    *have = need;
+    return true;
+  };
+  size_t nV_have = h->dV ? (size_t)d.batch * 4 : 0;
+  if (!ensure(&h->dA, &h->nA, nA) || !ensure(&h->dB, &h->nB, nB) || !ensure(&h->dD, &h->nD, nD) ||
+      !ensure(&h->dE, &h->nE, nE) || !ensure((void**)&h->dV, &nV_have, (size_t)d.batch * 4))
+    return fail(MBCI_ERR_NOMEM, "device scratch allocation failed");
+  if (nA && (e = cudaMemcpyAsync(h->dA, A, nA, cudaMemcpyHostToDevice, st)) != cudaSuccess) return cuda_fail(e, "H2D A");
+  if (nB && (e = cudaMemcpyAsync(h->dB, B, nB, cudaMemcpyHostToDevice, st)) != cudaSuccess) return cuda_fail(e, "H2D B");
+  if (nD && (e = cudaMemcpyAsync(h->dD, D, nD, cudaMemcpyHostToDevice, st)) != cudaSuccess) return cuda_fail(e, "H2D D");
+  const int32_t* dv = nullptr;
+  if (d.mask == MBCI_MASK_KEY_PADDING) {
+    if (!valid_len) return fail(MBCI_ERR_INVALID, "mask KEY_PADDING needs valid_len");
+    if ((e = cudaMemcpyAsync(h->dV, valid_len, d.batch * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess)
+      return cuda_fail(e, "H2D valid_len");
+    dv = h->dV;
+  }
+  mbci_status_t rs = launch(h, h->dA, h->dB, h->dD, h->dE, dv, st);
+  if (rs != MBCI_OK) return rs;
+  // E back row by row (2-D copies) so host bytes between rows are never overwritten
+  if (d.bs_e == d.M * d.ld_e) {
+    e = cudaMemcpy2DAsync(E, d.ld_e * s, h->dE, d.ld_e * s, d.L * s, d.batch * d.M, cudaMemcpyDeviceToHost, st);
+  } else {
+    for (int64_t b = 0; b < d.batch && e == cudaSuccess; ++b)
+      e = cudaMemcpy2DAsync((char*)E + b * d.bs_e * s, d.ld_e * s, (char*)h->dE + b * d.bs_e * s, d.ld_e * s,
+                            d.L * s, d.M, cudaMemcpyDeviceToHost, st);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "D2H E");
+  e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
+  return MBCI_OK;
+}
+
+mbci_status_t mbci_chain_destroy(mbci_chain_t h) {
+  if (!h) return MBCI_OK;
+  cudaFree(h->dA);
+  cudaFree(h->dB);
+  cudaFree(h->dD);
+  cudaFree(h->dE);
+  cudaFree(h->dV);
+  delete h;
+  return MBCI_OK;
+}
+
+mbci_status_t mbci_chain_plan(mbci_chain_t h, mbci_plan_t* out) {
+  if (!h || !out) return fail(MBCI_ERR_INVALID, "NULL argument");
+  *out = h->plan;
+  return MBCI_OK;
+}
+
+mbci_status_t mbci_chain_describe(mbci_chain_t h, char* buf, size_t len) {
+  if (!h || !buf || len == 0) return fail(MBCI_ERR_INVALID, "NULL argument");
+  const mbci_plan_t& p = h->plan;
+  snprintf(buf, len,
+           "kernel=%s BM=%d BN=%d TK=%d TL=%d stages=%d smem=%d tmem=%d n_block=%lld "
+           "t_estm=%.3gs alpha=%.4f t_b200=%.3gs",
+           p.kernel == 0 ? "tcgen05" : "simt", p.BM, p.BN, p.TK, p.TL, p.stages, p.smem_bytes, p.tmem_cols,
+           (long long)p.n_block, p.t_estm, p.alpha, p.t_b200);
+  return MBCI_OK;
+}
+
+int32_t mbci_chain_launches_per_run(mbci_chain_t h) {
+  if (!h) return 0;
+  return (h->d.batch == 0 || h->d.M == 0 || h->d.L == 0) ? 0 : 1;
+}
+
+const char* mbci_status_string(mbci_status_t s) {
+  switch (s) {
+    case MBCI_OK: return "MBCI_OK";
+    case MBCI_ERR_INVALID: return "MBCI_ERR_INVALID";
+    case MBCI_ERR_UNSUPPORTED: return "MBCI_ERR_UNSUPPORTED";
+    case MBCI_ERR_CUDA: return "MBCI_ERR_CUDA";
+    case MBCI_ERR_NOMEM: return "MBCI_ERR_NOMEM";
+  }
+  return "MBCI_ERR_?";
+}
+
+const char* mbci_last_error(void) { return g_err.c_str(); }
+
+int32_t mbci_abi_version(void) { return MBCI_ABI_VERSION; }
+
+void mbci_hw_default(mbci_hw_t* hw) {
+  if (hw) hw_default(hw);
+}
+
+mbci_status_t mbci_plan_enumerate(const mbci_chain_desc_t* desc, const mbci_hw_t* hw, mbci_plan_t* plans,
+                                  int32_t cap, int32_t* n_out) {
+  mbci_chain_desc_t d;
+  mbci_status_t s = normalize(desc, &d);
+  if (s != MBCI_OK) return s;
+  mbci_hw_t h;
+  if (hw) h = *hw; else hw_default(&h);
+  std::vector<mbci_plan_t> v;
+  enumerate_plans(d, h, v);
+  if (n_out) *n_out = (int32_t)v.size();
+  if (plans)
+    for (int32_t i = 0; i < cap && i < (int32_t)v.size(); ++i) plans[i] = v[i];
+  if (v.empty()) return fail(MBCI_ERR_UNSUPPORTED, "no legal plan");
+  return MBCI_OK;
+}
+
+mbci_status_t mbci_plan_select(const mbci_chain_desc_t* desc, const mbci_hw_t* hw, mbci_plan_t* out) {
+  if (!out) return fail(MBCI_ERR_INVALID, "out is NULL");
+  int32_t n = 0;
+  return mbci_plan_enumerate(desc, hw, out, 1, &n);
+}
+
+mbci_status_t mbci_model_terms(int64_t batch, int64_t M, int64_t N, int64_t K, int64_t L, int64_t TM,
+                               int64_t TN, int64_t TK, int64_t TH, int32_t elem_bytes, const mbci_hw_t* hw,
+                               double out[5]) {
+  if (!out || TM <= 0 || TN <= 0 || TK <= 0 || TH <= 0 || batch <= 0 || M < 0 || N < 0 || K < 0 || L < 0 ||
+      elem_bytes <= 0)
+    return fail(MBCI_ERR_INVALID, "bad model arguments");
+  mbci_hw_t h;
+  if (hw) h = *hw; else hw_default(&h);
+  model_terms(batch, M, N, K, L, TM, TN, TK, TH, elem_bytes, h, out);
+  return MBCI_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,22 @@
+// selector.h — host-side tile selector (see selector.cpp).
+#pragma once
+#include <cstdint>
+#include <vector>
+
+#include "../../include/mbci.h"
+
+namespace mbci {
+
+void model_terms(int64_t batch, int64_t M, int64_t N, int64_t K, int64_t L, int64_t TM,
+                 int64_t TN, int64_t TK, int64_t TH, int32_t s, const mbci_hw_t& hw,
+                 double out[5]);
+bool rule3_reject(int64_t size, int64_t tile);
+int64_t tc_smem_bytes(int32_t k_steps, int32_t BN, int32_t TL, int32_t stages, int32_t b_layout,
+                      int32_t* a_bytes, int32_t* b_stage, int32_t* d_stage);
+int32_t tmem_alloc_cols(int32_t BN, int32_t TL);
+bool tc_eligible(const mbci_chain_desc_t& d);
+int enumerate_plans(const mbci_chain_desc_t& d, const mbci_hw_t& hw,
+                    std::vector<mbci_plan_t>& out);
+void hw_default(mbci_hw_t* hw);
+
+}  // namespace mbci

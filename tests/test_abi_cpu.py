@@ -1,0 +1,155 @@
+"""C-ABI contract checks that need no GPU: the library loads, exports every symbol the
+header declares, validates descriptors, and its host-only tile selector reproduces the
+paper's model (oracle/model.py) and respects the B200 budgets."""
+import ctypes
+import math
+import os
+import re
+import subprocess
+
+import pytest
+
+from oracle import model
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "mbci.h")
+
+
+@pytest.fixture(scope="module")
+def m():
+    from paper_2506_22169_b200 import _build
+    _build.build()
+    from paper_2506_22169_b200 import mbci
+    return mbci
+
+
+def header_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(mbci_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_exports_every_header_symbol(m):
+    names = header_functions()
+    assert len(names) >= 14
+    out = subprocess.run(["nm", "-D", "--defined-only", m.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\b[TW] (mbci_\w+)", out))
+    missing = [n for n in names if n not in exported]
+    assert not missing, missing
+    for n in names:
+        assert hasattr(m._lib, n)
+    assert sorted(m.EXPORTED) == names
+
+
+def test_version_and_status_strings(m):
+    assert m.mbci_abi_version() == 1
+    assert m.mbci_status_string(0) == b"MBCI_OK"
+    assert m.mbci_status_string(2) == b"MBCI_ERR_UNSUPPORTED"
+
+
+def _create(m, d):
+    h = ctypes.c_void_p()
+    return m.mbci_chain_create(ctypes.byref(d) if d is not None else None, 0, ctypes.byref(h)), h
+
+
+def test_validation_errors(m):
+    assert _create(m, None)[0] == m.MBCI_ERR_INVALID
+    assert _create(m, m.make_desc(-1, 8, 8, 8, 8))[0] == m.MBCI_ERR_INVALID
+    d = m.make_desc(1, 8, 8, 8, 8)
+    d.dtype = 7
+    assert _create(m, d)[0] == m.MBCI_ERR_INVALID
+    d = m.make_desc(1, 8, 8, 8, 8, op="none", mask=True)
+    assert _create(m, d)[0] == m.MBCI_ERR_INVALID
+    assert _create(m, m.make_desc(1, 8, 8, 129, 8))[0] == m.MBCI_ERR_UNSUPPORTED
+    assert _create(m, m.make_desc(1, 8, 8, 64, 256))[0] == m.MBCI_ERR_UNSUPPORTED
+    d = m.make_desc(1, 8, 8, 16, 8, strides={"ld_a": 8})   # row stride shorter than the row
+    assert _create(m, d)[0] == m.MBCI_ERR_INVALID
+    assert b"stride" in m.mbci_last_error()
+    assert m.mbci_chain_run(None, None, None, None, None, None, None) == m.MBCI_ERR_INVALID
+    assert m.mbci_chain_destroy(None) == m.MBCI_OK
+
+
+def test_no_gpu_reports_cuda_error(m):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    st, h = _create(m, m.make_desc(2, 128, 128, 64, 64, "f16"))
+    assert st in (m.MBCI_ERR_CUDA, m.MBCI_ERR_INVALID)
+    assert not h.value
+
+
+# ---------------------------------------------------------------- selector vs paper model
+SHAPES = [(96, 512, 512, 64, 64), (128, 1024, 1024, 64, 64), (64, 2048, 2048, 16, 16),
+          (64, 2048, 2048, 128, 128), (1, 128, 128, 16, 16), (3, 1000, 777, 80, 80),
+          (8, 1024, 1024, 128, 128), (1, 512, 256, 64, 128)]
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+def test_model_terms_match_oracle(m, shape):
+    b, M, N, K, L = shape
+    hw = m.hw_default()
+    for TM, TN, TK, TH in [(128, 128, 64, 64), (128, 64, 16, 32), (64, 256, 128, 16), (16, 16, 16, 16),
+                           (256, 128, 32, 128)]:
+        got = m.model_terms(b, M, N, K, L, TM, TN, TK, TH, 2, hw)
+        ref = model.chain_estimate(b, M, N, K, L, TM, TN, TK, TH, 2, hw.W, hw.P, hw.n_sm)
+        for k in ("t_mem", "t_comp", "alpha", "t_estm", "n_block"):
+            assert got[k] == pytest.approx(ref[k], rel=1e-12), (k, TM, TN, TK, TH)
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("b_layout", [0, 1])
+def test_enumerated_plans_are_legal_and_scored(m, shape, b_layout):
+    b, M, N, K, L = shape
+    hw = m.hw_default()
+    d = m.make_desc(b, M, N, K, L, "bf16", "softmax", b_layout=b_layout)
+    st, plans = m.plan_enumerate(d, hw)
+    assert st == m.MBCI_OK and plans
+    lpad = max(16, math.ceil(L / 16) * 16)
+    rule3_ok = any(not model.rule3_reject(N, bn) for bn in (64, 128))
+    scores = [p.t_b200 for p in plans]
+    assert scores == sorted(scores)
+    b_inner = N if b_layout == 0 else K
+    if any(x % 8 for x in (K, b_inner, L)):        # TMA needs 16-byte row strides
+        assert [p.kernel for p in plans] == [1]
+        return
+    for p in plans:
+        assert p.kernel == 0 and p.BM == 128 and p.BN in (64, 128)
+        assert p.TL % 16 == 0 and 16 <= p.TL <= lpad
+        assert p.TK == max(16, math.ceil(K / 16) * 16)
+        assert p.smem_bytes <= hw.smem_max
+        assert 2 * p.BN + p.TL <= p.tmem_cols <= 512 and p.tmem_cols & (p.tmem_cols - 1) == 0
+        assert 2 <= p.stages <= 4
+        if rule3_ok:
+            assert not model.rule3_reject(N, p.BN)
+        ref = model.chain_estimate(b, M, N, K, L, 128, p.BN, p.TK, p.TL, 2, hw.W, hw.P, hw.n_sm)
+        assert p.t_estm == pytest.approx(ref["t_estm"], rel=1e-12)
+        assert p.alpha == pytest.approx(ref["alpha"], rel=1e-12)
+        assert p.n_block == b * math.ceil(M / 128) * math.ceil(L / p.TL)
+    best = m.mbci_plan_t()
+    assert m.mbci_plan_select(ctypes.byref(d), ctypes.byref(hw), ctypes.byref(best)) == m.MBCI_OK
+    assert best.t_b200 == plans[0].t_b200
+
+
+def test_bert_base_prefers_full_L_tile(m):
+    """Chunking L onto the grid recomputes C; with 384 CTAs already
+    filling the GPU the selector keeps T_H = L."""
+    d = m.make_desc(96, 512, 512, 64, 64, "f16", "softmax")
+    p = m.mbci_plan_t()
+    assert m.mbci_plan_select(ctypes.byref(d), None, ctypes.byref(p)) == m.MBCI_OK
+    assert p.TL == 64 and p.kernel == 0
+
+
+def test_fp32_and_misaligned_go_to_cuda_cores(m):
+    st, plans = m.plan_enumerate(m.make_desc(1, 128, 128, 16, 16, "f32", "none"))
+    assert st == m.MBCI_OK and [p.kernel for p in plans] == [1]
+    st, plans = m.plan_enumerate(m.make_desc(2, 3, 5, 3, 3, "f16", "none"))   # K=3: 6-byte rows
+    assert st == m.MBCI_OK and plans[0].kernel == 1
+    st, plans = m.plan_enumerate(m.make_desc(1, 16, 10**6, 16, 16, "f32", "none"))  # C row > SMEM
+    assert st == m.MBCI_ERR_UNSUPPORTED and plans == []
+
+
+def test_rule3_fallback_keeps_a_plan_on_ragged_N(m):
+    """N = 300: every BN pads >= 5 % (Rule 3 rejects all); the selector then skips the rule."""
+    st, plans = m.plan_enumerate(m.make_desc(2, 200, 300, 64, 64, "bf16"))
+    assert st == m.MBCI_OK and plans
+    assert all(model.rule3_reject(300, p.BN) for p in plans)
