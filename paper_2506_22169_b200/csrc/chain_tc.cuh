@@ -67,8 +67,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* kv_empty = d_full + S;
   uint64_t* s_full = kv_empty + S;  // [2]
   uint64_t* p_full = s_full + 2;    // [2]
-  uint64_t* o_done = p_full + 2;    // [1]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 1);
+  uint64_t* o_done = p_full + 2;    // [1] one completion per G2(i)
+  uint64_t* o_final = o_done + 1;   // [1] one completion after the last G2
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_final + 1);
 
   const int warp = threadIdx.x >> 5;
   const int unit = blockIdx.x;
@@ -94,6 +95,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_init(&p_full[b], kRowThreads);
     }
     ptx::mbar_init(o_done, 1);
+    ptx::mbar_init(o_final, 1);
     ptx::fence_mbar_init();
     if (nt > 0) {  // maps are only encoded when the operands exist
       if (p.k_steps > 0) {
@@ -181,6 +183,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           ptx::mma_commit(&kv_empty[s]);
           ptx::mma_commit(o_done);
+          if (i == nt - 1) ptx::mma_commit(o_final);
         }
       }
     }
@@ -236,7 +239,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             const float alpha = ptx::ex2(m_run - m_new);
             l_run *= alpha;
             m_run = m_new;
-            ptx::mbar_wait(o_done, (j - 1) & 1);  // G2(j-1) has landed in O
+            // G2(j-1) has landed in O.  Parity waits are only unambiguous one phase ahead:
+            // s_full(j) completing implies G2(j-2) completed (tcgen05 ops retire in issue
+            // order), so o_done has completed j-1 or j times here.
+            ptx::mbar_wait(o_done, (j - 1) & 1);
             ptx::tc_fence_after();
             for (int c0 = 0; c0 < TLP; c0 += 16) {
               uint32_t r[16];
@@ -278,7 +284,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     // ------------------------------------------------------------ epilogue
     if (nt > 0) {
-      ptx::mbar_wait(o_done, (nt - 1) & 1);
+      // o_done may still be two phases behind here, so the last G2 has its own barrier.
+      ptx::mbar_wait(o_final, 0);
       ptx::tc_fence_after();
     }
     const float inv = (p.op == 2) ? (l_run > 0.f ? 1.0f / l_run : 0.f) : 1.0f;
