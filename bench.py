@@ -1,0 +1,410 @@
+#!/usr/bin/env python
+"""Benchmark of the fused MBCI chain (BASELINE.json metric) — one JSON line on rank 0.
+
+Default workload (N = 1): BASELINE.json configs[1], BERT-base self-attention chain,
+batch 8 x 12 heads, seq 512, head_dim 64, fp16, scale 1/8 + softmax.
+A "step" is one fused-chain launch over the whole batch (every §8(a) row on the path).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl {cuda,reference}]
+                    [--config C2|C3|C4-16|...|C6] [--no-cpu-baseline]
+
+Multi-GPU (torchrun, one rank per GPU): weak scaling — every rank runs the full
+per-GPU batch of the config on its own shard of β; no collective on the
+data path; NCCL only for the barrier and the MAX over ranks of device time.
+
+Timing: inputs resident in HBM; `rot` sets of (A, B, D, E) used round-robin so the
+working set between reuses exceeds 2x L2 (126 MB) — no step hits L2-resident inputs;
+the K steps are captured once in a CUDA graph and replayed on a dedicated stream,
+bracketed by CUDA events on that stream (plus barrier + synchronize); max over ranks.
+`e2e` times mbci_chain_run_host (pinned host buffers, H2D inputs + D2H E every step).
+`--impl reference` times the CPU oracle (oracle/) on a bounded sample of the same
+workload (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fused-chain µs and HBM GB/s (% of B200 peak), BERT-base attn, 1/2/4/8 GPU"
+
+# name: (dtype, batch x heads, M, N, K, L, op, description)
+CONFIGS = {
+    "C1": ("f32", 1, 128, 128, 16, 16, "none", "fp32 chain E=(A.B).D, batch 1, M=N=128, K=L=16, no inter-op"),
+    "C2": ("f16", 96, 512, 512, 64, 64, "softmax",
+           "BERT-base self-attention chain fp16: batch 8 x 12 heads, seq 512, head_dim 64, scale 1/8 + softmax"),
+    "C3": ("bf16", 128, 1024, 1024, 64, 64, "softmax",
+           "BERT-large attention chain bf16: batch 8 x 16 heads, seq 1024, head_dim 64, scale+softmax"),
+    "C4-16": ("bf16", 64, 2048, 2048, 16, 16, "none", "plain chain bf16: batch 64, M=N=2048, K=L=16"),
+    "C4-32": ("bf16", 64, 2048, 2048, 32, 32, "none", "plain chain bf16: batch 64, M=N=2048, K=L=32"),
+    "C4-64": ("bf16", 64, 2048, 2048, 64, 64, "none", "plain chain bf16: batch 64, M=N=2048, K=L=64"),
+    "C4-128": ("bf16", 64, 2048, 2048, 128, 128, "none", "plain chain bf16: batch 64, M=N=2048, K=L=128"),
+    "C5": ("bf16", 512, 4096, 4096, 128, 128, "softmax",
+           "long-sequence attention chain bf16: batch 32 x 16 heads, seq 4096, head_dim 128"),
+    "C6": ("f16", 96, 256, 256, 64, 64, "softmax", "ViT-base attention chain fp16: batch 8 x 12 heads, seq 256, d 64"),
+}
+
+L2_BYTES = 126 * 1024 * 1024
+
+
+def peaks():
+    p = {"hbm_gbs": None, "bf16_tflops": None, "bf16_tflops_sustained": None, "src": "fallback"}
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            j = json.load(f)
+        p.update({k: j.get(k) for k in ("hbm_gbs", "bf16_tflops", "bf16_tflops_sustained")})
+        p["src"] = "measured (MEASURED_PEAKS.json)"
+    if p["hbm_gbs"] is None:   # B200_PROFILING.md fallback
+        p.update(hbm_gbs=6650.0, bf16_tflops=1590.0, bf16_tflops_sustained=1400.0, src="fallback (B200_PROFILING.md)")
+    return p
+
+
+def cfg_numbers(name):
+    dtype, b, M, N, K, L, op, desc = CONFIGS[name]
+    s = 4 if dtype == "f32" else 2
+    bytes_ = b * (M * K + K * N + N * L + M * L) * s       # A, B, D, E only
+    flops = 2.0 * b * M * N * (K + L)
+    exps = b * M * N if op == "softmax" else 0
+    return dtype, b, M, N, K, L, op, desc, s, bytes_, flops, exps
+
+
+# ---------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_id):
+        self.gpu_id = gpu_id
+        self.rows = []
+        self.proc = None
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "100", "-i", str(self.gpu_id)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append((time.time(), [x.strip() for x in line.split(",")]))
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.t:
+            self.t.join(timeout=2)
+
+    def summary(self, t0, t1):
+        rows = [r for (t, r) in self.rows if t0 <= t <= t1 + 0.15] or [r for (_, r) in self.rows]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [num(r[1]) for r in rows if len(r) > 2 and num(r[1]) is not None]
+        smax = [num(r[2]) for r in rows if len(r) > 2 and num(r[2]) is not None]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for i, n in enumerate(names):
+                if len(r) > 5 + i and r[5 + i].lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(rows),
+                "power_w_max": max((num(r[3]) or 0.0) for r in rows) if rows else None}
+
+
+# ---------------------------------------------------------------------------- CPU oracle
+def time_oracle(name, min_seconds, max_slices=None, seed=0):
+    """Oracle on a bounded sample (a few β slices of the workload); returns (GB/s, sample, cores, secs)."""
+    import mbci_inputs as gen
+    import oracle
+    dtype, b, M, N, K, L, op, desc, s, bytes_, flops, exps = cfg_numbers(name)
+    per_slice = (M * K + K * N + N * L + M * L) * s
+    cores = oracle.max_threads()
+    nsl = max_slices or max(1, min(b, cores))
+    inp = gen.make_chain_inputs(seed, dtype, nsl, M, N, K, L, 1 if op == "softmax" else 0)
+    sc = 1.0 / math.sqrt(K) if op == "softmax" else 1.0
+    oracle.chain(inp, op, sc)                      # warm (page-in)
+    t0 = time.perf_counter()
+    reps = 0
+    while True:
+        oracle.chain(inp, op, sc)
+        reps += 1
+        el = time.perf_counter() - t0
+        if el >= min_seconds:
+            break
+    sec_per = el / reps
+    gbs = nsl * per_slice / sec_per / 1e9
+    sample = f"{nsl} of {b} batch x head slices of {name} per step (fp64 unfused chain, {reps} reps, {el:.1f} s)"
+    return gbs, sample, cores, sec_per
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle as it stands, on rank 0 only."""
+    if rank != 0:
+        return
+    name = args.config
+    dtype, b, M, N, K, L, op, desc, s, bytes_, flops, exps = cfg_numbers(name)
+    import mbci_inputs as gen
+    import oracle
+    cores = oracle.max_threads()
+    nsl = max(1, min(b, cores))           # bounded sample per step
+    per_slice = (M * K + K * N + N * L + M * L) * s
+    inp = gen.make_chain_inputs(0, dtype, nsl, M, N, K, L, 1 if op == "softmax" else 0)
+    sc = 1.0 / math.sqrt(K) if op == "softmax" else 1.0
+    for _ in range(args.warmup):
+        oracle.chain(inp, op, sc)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.chain(inp, op, sc)
+    el = time.perf_counter() - t0
+    ms = el / args.steps * 1e3
+    gbs = nsl * per_slice / (el / args.steps) / 1e9
+    sample = f"{nsl} of {b} batch x head slices of {name} per step (fp64 unfused chain)"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": desc, "name": name, "batch_heads": b, "M": M, "N": N, "K": K, "L": L, "op": op,
+                   "sample_batch_heads_per_step": nsl, "parallelism": "host cores (OpenMP)"},
+        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------- CUDA path
+def run_cuda(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import mbci_inputs as gen
+    from paper_2506_22169_b200 import mbci, sharding
+
+    name = args.config
+    dtype, b, M, N, K, L, op, desc, s, bytes_, flops, exps = cfg_numbers(name)
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    tdt = {"f32": torch.float32, "f16": torch.float16, "bf16": torch.bfloat16}[dtype]
+    b_layout = 1 if op == "softmax" else 0
+    sc = 1.0 / math.sqrt(K) if op == "softmax" else 1.0
+    sig = (1.0, 1.0, 1.0) if op == "softmax" else (1.0, 1.0 / math.sqrt(K), 1.0 / math.sqrt(N))
+
+    # this rank's shard of a weak-scaling global batch of b * world
+    lo, hi = sharding.shard_range(b * world, rank, world)
+    nb = hi - lo
+    inp = gen.make_chain_inputs(args.seed, dtype, nb, M, N, K, L, b_layout, sigmas=sig, batch_start=lo)
+
+    def to_t(bits):
+        x = torch.from_numpy(bits.view(np.int32 if dtype == "f32" else np.int16))
+        return x.view(tdt)
+
+    hA, hB, hD = to_t(inp.A), to_t(inp.B), to_t(inp.D)
+    step_bytes = nb * (M * K + K * N + N * L + M * L) * s
+    rot = max(2, math.ceil(2 * L2_BYTES / step_bytes) + 1)
+    rot = min(rot, max(2, int(0.5 * torch.cuda.mem_get_info(dev)[0] // max(step_bytes, 1))))
+    sets = []
+    for r in range(rot):
+        A, B, D = hA.to(dev), hB.to(dev), hD.to(dev)
+        E = torch.empty(nb, M, L, dtype=tdt, device=dev)
+        sets.append((A, B, D, E))
+    forced = None
+    if args.plan:
+        forced = mbci.mbci_plan_t()
+        forced.kernel = 0
+        forced.BN, forced.TL, forced.stages = (int(x) for x in args.plan.split(":"))
+    ch = mbci.Chain(nb, M, N, K, L, dtype, op, sc, b_layout=b_layout, device=local_rank, tune=args.tune,
+                    plan=forced)
+    plan = ch.plan()
+    launches = ch.launches_per_run()
+    stream = torch.cuda.Stream(dev)
+
+    def step(i):
+        A, B, D, E = sets[i % rot]
+        ch.run_ptr(A.data_ptr(), B.data_ptr(), D.data_ptr(), E.data_ptr(), 0, stream.cuda_stream)
+
+    # warm-up (eager), then capture exactly K steps in one graph
+    with torch.cuda.stream(stream):
+        for i in range(args.warmup):
+            step(i)
+    stream.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        for i in range(args.steps):
+            step(i)
+    # sustained pre-run (not timed) so the clock sampler sees the kernel under load
+    sampler = ClockSampler(_gpu_id(local_rank))
+    sampler.start()
+    time.sleep(0.3)
+    t_load0 = time.time()
+    pre_t0 = time.perf_counter()
+    while time.perf_counter() - pre_t0 < args.sustain:
+        with torch.cuda.stream(stream):
+            g.replay()
+        stream.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    with torch.cuda.stream(stream):
+        g.replay()
+    ev1.record(stream)
+    ev1.synchronize()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t_load1 = time.time()
+    time.sleep(0.25)
+    sampler.stop()
+    ms_local = ev0.elapsed_time(ev1)
+    ms = sharding.max_over_ranks(ms_local)
+    ms_per_step = ms / args.steps
+    total_bytes = sharding.sum_over_ranks(step_bytes)
+    gbs = total_bytes / (ms_per_step * 1e-3) / 1e9
+    clocks = sampler.summary(t_load0, t_load1)
+
+    # ---- e2e through the public host entry point (pinned host buffers)
+    pA, pB, pD = hA.pin_memory(), hB.pin_memory(), hD.pin_memory()
+    pE = torch.empty(nb, M, L, dtype=tdt).pin_memory()
+    e2e_steps = max(3, min(args.steps, 20))
+    for _ in range(2):
+        ch.run_host(pA, pB, pD, pE, stream=stream)
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        ch.run_host(pA, pB, pD, pE, stream=stream)
+    e1.record(stream)
+    e1.synchronize()
+    e2e_ms = sharding.max_over_ranks(e0.elapsed_time(e1) / e2e_steps)
+    h2d = (hA.numel() + hB.numel() + hD.numel()) * s
+    d2h = pE.numel() * s
+    e2e_gbs = total_bytes / (e2e_ms * 1e-3) / 1e9
+
+    if rank != 0:
+        return
+    pk = peaks()
+    tflops = world * nb / b * flops / (ms_per_step * 1e-3) / 1e12 if b else 0.0
+    frac = gbs / (pk["hbm_gbs"] * world)
+    traffic = _traffic(name, world)
+    roofline = {"bound": "hbm", "achieved": gbs / world, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": frac, "traffic": traffic, "peak_src": pk["src"],
+                "kernel": "k_chain_tc" if plan.kernel == 0 else "k_chain_simt",
+                "per_launch_bytes": step_bytes, "per_launch_us": ms_per_step * 1e3,
+                "tensor_tflops": tflops / world, "tensor_frac": tflops / world / pk["bf16_tflops"],
+                "ex2_per_s": (exps * nb / b) / (ms_per_step * 1e-3) if exps else 0.0}
+    if not args.no_cpu_baseline and world == 1:
+        cgbs, sample, cores, _ = time_oracle(name, args.cpu_seconds)
+        cpu = {"value": cgbs, "unit": "GB/s", "cores": cores, "kind": "oracle", "sample": sample}
+    else:
+        cpu = None
+    line = {
+        "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "us_per_chain": ms_per_step * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dtype, "data": "synthetic",
+        "config": {"workload": desc, "name": name, "batch_heads_per_gpu": b, "global_batch_heads": b * world,
+                   "M": M, "N": N, "K": K, "L": L, "op": op, "scale": sc, "b_layout": b_layout,
+                   "l2": f"{rot} rotating input sets ({rot * step_bytes / 2**20:.0f} MiB) > 2x L2 between reuses",
+                   "timing": "K steps in one CUDA graph, CUDA events on the launch stream, max over ranks",
+                   "parallelism": f"dp{world} (batch x head sharding, no data-path collective)",
+                   "plan": ch.describe()},
+        "hbm_frac_of_8TBps": gbs / (8000.0 * world),
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_gbs, "unit": "GB/s", "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "api": "mbci_chain_run_host"},
+        "gpu_launches": launches * args.steps,
+        "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+    ch.close()
+
+
+def _gpu_id(local_rank):
+    try:
+        import torch
+        u = str(torch.cuda.get_device_properties(local_rank).uuid)
+        return u if u.startswith("GPU-") else "GPU-" + u
+    except Exception:
+        return local_rank
+
+
+def _traffic(name, world):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(path):
+        return None
+    try:
+        with open(path) as f:
+            j = json.load(f)
+        v = j.get(name)
+        return v.get("dram_bytes_per_launch") if isinstance(v, dict) else v
+    except Exception:
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["cuda", "reference"], default="cuda")
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--tune", type=int, default=0)
+    ap.add_argument("--plan", default="", help="force a plan BN:TL:stages (tensor-core path)")
+    ap.add_argument("--sustain", type=float, default=1.0, help="seconds of untimed load for the clock sampler")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus != world and world > 1:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_cuda(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

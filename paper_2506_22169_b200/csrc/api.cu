@@ -156,6 +156,7 @@ struct mbci_chain {
   int32_t kch = 1, dch = 1;
   MapCacheEntry cache[8];
   uint64_t stamp = 0;
+  uint64_t* trace = nullptr;
   // end-to-end scratch
   void *dA = nullptr, *dB = nullptr, *dD = nullptr, *dE = nullptr;
   int32_t* dV = nullptr;
@@ -266,6 +267,7 @@ mbci_status_t launch(mbci_chain* h, const void* A, const void* B, const void* D,
     TcParams t = h->tp;
     t.valid_len = vl;
     t.E = E;
+    t.trace = h->trace;
     h->tc<<<(unsigned)h->plan.n_block, kThreads, h->plan.smem_bytes, st>>>(ent->ta, ent->tb, ent->td, t);
   } else {
     SimtParams sp{};
@@ -528,6 +530,14 @@ mbci_status_t mbci_chain_describe(mbci_chain_t h, char* buf, size_t len) {
            "t_estm=%.3gs alpha=%.4f t_b200=%.3gs",
            p.kernel == 0 ? "tcgen05" : "simt", p.BM, p.BN, p.TK, p.TL, p.stages, p.smem_bytes, p.tmem_cols,
            (long long)p.n_block, p.t_estm, p.alpha, p.t_b200);
+  return MBCI_OK;
+}
+
+mbci_status_t mbci_chain_set_trace(mbci_chain_t h, void* buf, int64_t cap_bytes) {
+  if (!h) return fail(MBCI_ERR_INVALID, "handle is NULL");
+  if (buf && cap_bytes < h->plan.n_block * 64 * 8)
+    return fail(MBCI_ERR_INVALID, "trace buffer needs %lld bytes", (long long)(h->plan.n_block * 64 * 8));
+  h->trace = static_cast<uint64_t*>(buf);
   return MBCI_OK;
 }
 

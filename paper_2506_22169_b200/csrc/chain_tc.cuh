@@ -7,11 +7,13 @@
 // intermediate C never leaves the SM: S = A·B_j lands in tensor memory, the inter-GEMM op
 // turns it into P (16-bit) in place, and GEMM2 reads P straight from tensor memory.
 //
-// Warp roles (192 threads):
+// Warp roles (224 threads):
 //   warps 0-3  "row warps": thread t owns output row t (TMEM lane t); softmax / scale /
 //              convert of S_j into P_j, lazy O rescale, epilogue (E = O / l).
-//   warp 4     TMA producer: A once, then B_j and D_j into a `stages`-deep SMEM ring.
+//   warp 4     TMA producer: A once, then B_j into a `stages`-deep SMEM ring.
 //   warp 5     tcgen05 issuer (one elected lane) + TMEM allocator.
+//   warp 6     TMA producer: D_j into its own `stages`-deep ring (B and D slots are
+//              released separately: B_j after G1(j), D_j after G2(j)).
 // Issue order of the MMA warp: G1(0) G1(1) G2(0) G1(2) G2(1) ... G2(nt-1), so the row
 // warps convert S_j while the tensor core runs G2(j-1) and G1(j+1) (S double-buffered).
 //
@@ -43,14 +45,21 @@ struct TcParams {
   uint32_t kp_rows;        // B (layout 0) box rows = 16 * k_steps
   uint32_t tmem_cols;
   uint32_t idesc1, idesc2;
+  uint64_t* trace;   // optional per-CTA event timestamps (debug; see mbci_chain_set_trace)
+};
+
+// Trace slots (64 x u64 per CTA, globaltimer ns unless noted).
+enum : int {
+  kTrStart = 0, kTrSetup = 1, kTrSmid = 2, kTrTileS = 3 /* +2j */, kTrTileP = 4 /* +2j */,
+  kTrEpi = 40, kTrEnd = 41, kTrAFull = 42, kTrBFull = 43 /* +j, j < 8 */, kTrTiles = 16
 };
 
 constexpr int kRowThreads = 128;
-constexpr int kThreads = 192;
+constexpr int kThreads = 224;
 constexpr float kRescaleTau = 8.0f;   // lazy rescale threshold, log2 units (P <= 2^8)
 
 template <bool BF16, int BN, int KCH, int BL, int DCH>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, BN == 64 ? 2 : 1)
     k_chain_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const __grid_constant__ CUtensorMap tmD, const TcParams p) {
   extern __shared__ uint8_t smem_raw[];
@@ -64,8 +73,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* a_full = bars;
   uint64_t* b_full = bars + 1;
   uint64_t* d_full = b_full + S;
-  uint64_t* kv_empty = d_full + S;
-  uint64_t* s_full = kv_empty + S;  // [2]
+  uint64_t* b_empty = d_full + S;   // B_j's slot is free once G1(j) has read it
+  uint64_t* d_empty = b_empty + S;  // D_j's slot is free once G2(j) has read it
+  uint64_t* s_full = d_empty + S;   // [2]
   uint64_t* p_full = s_full + 2;    // [2]
   uint64_t* o_done = p_full + 2;    // [1] one completion per G2(i)
   uint64_t* o_final = o_done + 1;   // [1] one completion after the last G2
@@ -73,6 +83,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int unit = blockIdx.x;
+  uint64_t* tr = p.trace ? p.trace + static_cast<int64_t>(blockIdx.x) * 64 : nullptr;
+  if (tr && threadIdx.x == 0) {
+    tr[kTrStart] = ptx::globaltimer();
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    tr[kTrSmid] = smid;
+  }
   const int ht = unit % p.l_h;
   const int mt = (unit / p.l_h) % p.l_m;
   const int beta = unit / (p.l_h * p.l_m);
@@ -88,7 +105,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < S; ++s) {
       ptx::mbar_init(&b_full[s], 1);
       ptx::mbar_init(&d_full[s], 1);
-      ptx::mbar_init(&kv_empty[s], 1);
+      ptx::mbar_init(&b_empty[s], 1);
+      ptx::mbar_init(&d_empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&s_full[b], 1);
@@ -110,33 +128,36 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (tr && threadIdx.x == 0) tr[kTrSetup] = ptx::globaltimer();
 
   if (warp == 4) {
-    // ------------------------------------------------------------ TMA producer
-    if (ptx::elect_one() && nt > 0) {
-      if (p.k_steps > 0) {
-        ptx::mbar_arrive_expect_tx(a_full, p.a_bytes);
+    // ------------------------------------------------------------ TMA producer: A, B_j
+    if (ptx::elect_one() && nt > 0 && p.k_steps > 0) {
+      ptx::mbar_arrive_expect_tx(a_full, p.a_bytes);
 #pragma unroll
-        for (int c = 0; c < KCH; ++c)
-          ptx::tma_load_3d(sA + c * 16384, &tmA, a_full, c * 64, m0, beta);
-      }
+      for (int c = 0; c < KCH; ++c) ptx::tma_load_3d(sA + c * 16384, &tmA, a_full, c * 64, m0, beta);
       for (int j = 0; j < nt; ++j) {
         const int s = j % S;
-        if (j >= S) ptx::mbar_wait(&kv_empty[s], ((j / S) - 1) & 1);
-        if (p.k_steps > 0) {
-          uint8_t* dst = sB + s * p.b_stage_bytes;
-          ptx::mbar_arrive_expect_tx(&b_full[s], p.b_stage_bytes);
-          if constexpr (BL == 1) {
+        if (j >= S) ptx::mbar_wait(&b_empty[s], ((j / S) - 1) & 1);
+        uint8_t* dst = sB + s * p.b_stage_bytes;
+        ptx::mbar_arrive_expect_tx(&b_full[s], p.b_stage_bytes);
+        if constexpr (BL == 1) {
 #pragma unroll
-            for (int c = 0; c < KCH; ++c)
-              ptx::tma_load_3d(dst + c * (BN * 128), &tmB, &b_full[s], c * 64, j * BN, beta);
-          } else {
+          for (int c = 0; c < KCH; ++c)
+            ptx::tma_load_3d(dst + c * (BN * 128), &tmB, &b_full[s], c * 64, j * BN, beta);
+        } else {
 #pragma unroll
-            for (int c = 0; c < BN / 64; ++c)
-              ptx::tma_load_3d(dst + c * (p.kp_rows * 128), &tmB, &b_full[s], j * BN + c * 64, 0,
-                               beta);
-          }
+          for (int c = 0; c < BN / 64; ++c)
+            ptx::tma_load_3d(dst + c * (p.kp_rows * 128), &tmB, &b_full[s], j * BN + c * 64, 0, beta);
         }
+      }
+    }
+  } else if (warp == 6) {
+    // ------------------------------------------------------------ TMA producer: D_j
+    if (ptx::elect_one() && nt > 0) {
+      for (int j = 0; j < nt; ++j) {
+        const int s = j % S;
+        if (j >= S) ptx::mbar_wait(&d_empty[s], ((j / S) - 1) & 1);
         uint8_t* ddst = sD + s * p.d_stage_bytes;
         ptx::mbar_arrive_expect_tx(&d_full[s], p.d_stage_bytes);
 #pragma unroll
@@ -149,12 +170,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (ptx::elect_one() && nt > 0) {
       const uint32_t tO = tmem + 2 * BN;
       if (p.k_steps > 0) ptx::mbar_wait(a_full, 0);
+      if (tr) tr[kTrAFull] = ptx::globaltimer();
       const uint32_t a_base = ptx::smem_u32(sA);
       for (int j = 0; j <= nt; ++j) {
         if (j < nt) {
           const int s = j % S, buf = j & 1;
           if (p.k_steps > 0) {
             ptx::mbar_wait(&b_full[s], (j / S) & 1);
+            if (tr && j < 8) tr[kTrBFull + j] = ptx::globaltimer();
             ptx::tc_fence_after();
             const uint32_t b_base = ptx::smem_u32(sB + s * p.b_stage_bytes);
             for (int ks = 0; ks < p.k_steps; ++ks) {
@@ -167,6 +190,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 bd = ptx::sdesc_sw128(b_base + ks * 2048, p.kp_rows * 128, 1024);
               ptx::mma_ss(tmem + buf * BN, ad, bd, p.idesc1, ks > 0 ? 1u : 0u);
             }
+            ptx::mma_commit(&b_empty[s]);
           }
           ptx::mma_commit(&s_full[buf]);
         }
@@ -181,7 +205,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t dd = ptx::sdesc_sw128(d_base + ks * 2048, BN * 128, 1024);
             ptx::mma_ts(tO, tmem + buf * BN + ks * 8, dd, p.idesc2, (i > 0 || ks > 0) ? 1u : 0u);
           }
-          ptx::mma_commit(&kv_empty[s]);
+          ptx::mma_commit(&d_empty[s]);
           ptx::mma_commit(o_done);
           if (i == nt - 1) ptx::mma_commit(o_final);
         }
@@ -200,6 +224,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int j = 0; j < nt; ++j) {
       const int buf = j & 1;
       ptx::mbar_wait(&s_full[buf], (j >> 1) & 1);
+      if (tr && threadIdx.x == 0 && j < kTrTiles) tr[kTrTileS + 2 * j] = ptx::globaltimer();
       ptx::tc_fence_after();
       uint32_t sr[BN];
       if (p.k_steps > 0) {
@@ -219,14 +244,32 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool full = valid >= BN;
         // tile max of z = sc * S over valid keys (sc >= 0: max S; sc < 0: min S)
         float mx;
-        if (sc >= 0.f) {
+        if (full) {
+          if (sc >= 0.f) {
+            float m0v = s[0], m1v = s[1];
+#pragma unroll
+            for (int c = 2; c + 3 < BN; c += 4) {
+              m0v = ptx::max3(m0v, s[c], s[c + 1]);
+              m1v = ptx::max3(m1v, s[c + 2], s[c + 3]);
+            }
+            mx = ptx::max3(m0v, m1v, ptx::max3(s[BN - 2], s[BN - 1], s[0]));
+          } else {
+            float m0v = s[0], m1v = s[1];
+#pragma unroll
+            for (int c = 2; c + 3 < BN; c += 4) {
+              m0v = ptx::min3(m0v, s[c], s[c + 1]);
+              m1v = ptx::min3(m1v, s[c + 2], s[c + 3]);
+            }
+            mx = ptx::min3(m0v, m1v, ptx::min3(s[BN - 2], s[BN - 1], s[0]));
+          }
+        } else if (sc >= 0.f) {
           mx = -INFINITY;
 #pragma unroll
-          for (int c = 0; c < BN; ++c) mx = (full || c < valid) ? fmaxf(mx, s[c]) : mx;
+          for (int c = 0; c < BN; ++c) mx = (c < valid) ? fmaxf(mx, s[c]) : mx;
         } else {
           mx = INFINITY;
 #pragma unroll
-          for (int c = 0; c < BN; ++c) mx = (full || c < valid) ? fminf(mx, s[c]) : mx;
+          for (int c = 0; c < BN; ++c) mx = (c < valid) ? fminf(mx, s[c]) : mx;
         }
         const float m_tile = mx * sc;
         if (j == 0) {
@@ -280,6 +323,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::tmem_wait_st();
       ptx::tc_fence_before();
       ptx::mbar_arrive(&p_full[buf]);
+      if (tr && threadIdx.x == 0 && j < kTrTiles) tr[kTrTileP + 2 * j] = ptx::globaltimer();
     }
 
     // ------------------------------------------------------------ epilogue
@@ -288,6 +332,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_wait(o_final, 0);
       ptx::tc_fence_after();
     }
+    if (tr && threadIdx.x == 0) tr[kTrEpi] = ptx::globaltimer();
     const float inv = (p.op == 2) ? (l_run > 0.f ? 1.0f / l_run : 0.f) : 1.0f;
     const int gm = m0 + row;
     const int ncols = min(TLP, p.L - h0);
@@ -322,6 +367,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   ptx::tc_fence_before();
   __syncthreads();
+  if (tr && threadIdx.x == 0) tr[kTrEnd] = ptx::globaltimer();
   if (warp == 5) {
     __syncwarp();
     ptx::tc_fence_after();

@@ -73,7 +73,7 @@ int64_t tc_smem_bytes(int32_t k_steps, int32_t BN, int32_t TL, int32_t stages, i
   if (a_bytes) *a_bytes = a;
   if (b_stage) *b_stage = b;
   if (d_stage) *d_stage = d;
-  const int32_t n_bars = 1 + 3 * stages + 4 + 2;
+  const int32_t n_bars = 1 + 4 * stages + 4 + 2;
   return static_cast<int64_t>(a) + static_cast<int64_t>(stages) * (b + d) + 8 * n_bars + 16 +
          1024;  // + alignment slack for the 1024-B swizzle atoms
 }

@@ -67,6 +67,7 @@ _lib.mbci_chain_run_host.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _vp]
 _lib.mbci_chain_destroy.argtypes = [_vp]
 _lib.mbci_chain_plan.argtypes = [_vp, _P(mbci_plan_t)]
 _lib.mbci_chain_describe.argtypes = [_vp, ctypes.c_char_p, ctypes.c_size_t]
+_lib.mbci_chain_set_trace.argtypes = [_vp, _vp, ctypes.c_int64]
 _lib.mbci_chain_launches_per_run.argtypes = [_vp]
 _lib.mbci_chain_launches_per_run.restype = ctypes.c_int32
 _lib.mbci_status_string.argtypes = [ctypes.c_int]
@@ -80,12 +81,14 @@ _lib.mbci_plan_enumerate.argtypes = [_P(mbci_chain_desc_t), _P(mbci_hw_t), _P(mb
 _lib.mbci_plan_select.argtypes = [_P(mbci_chain_desc_t), _P(mbci_hw_t), _P(mbci_plan_t)]
 _lib.mbci_model_terms.argtypes = [ctypes.c_int64] * 9 + [ctypes.c_int32, _P(mbci_hw_t), _P(ctypes.c_double)]
 for _f in ("mbci_chain_create", "mbci_chain_create_with_plan", "mbci_chain_run", "mbci_chain_run_host",
+           "mbci_chain_set_trace",
            "mbci_chain_destroy", "mbci_chain_plan", "mbci_chain_describe", "mbci_plan_enumerate",
            "mbci_plan_select", "mbci_model_terms"):
     getattr(_lib, _f).restype = _st
 
 EXPORTED = ["mbci_chain_create", "mbci_chain_create_with_plan", "mbci_chain_run", "mbci_chain_run_host",
             "mbci_chain_destroy", "mbci_chain_plan", "mbci_chain_describe", "mbci_chain_launches_per_run",
+            "mbci_chain_set_trace",
             "mbci_status_string", "mbci_last_error", "mbci_abi_version", "mbci_hw_default",
             "mbci_plan_enumerate", "mbci_plan_select", "mbci_model_terms"]
 
@@ -98,6 +101,7 @@ mbci_chain_destroy = _lib.mbci_chain_destroy
 mbci_chain_plan = _lib.mbci_chain_plan
 mbci_chain_describe = _lib.mbci_chain_describe
 mbci_chain_launches_per_run = _lib.mbci_chain_launches_per_run
+mbci_chain_set_trace = _lib.mbci_chain_set_trace
 mbci_status_string = _lib.mbci_status_string
 mbci_last_error = _lib.mbci_last_error
 mbci_abi_version = _lib.mbci_abi_version
@@ -190,6 +194,13 @@ class Chain:
         buf = ctypes.create_string_buffer(512)
         check(mbci_chain_describe(self.h, buf, 512), "mbci_chain_describe")
         return buf.value.decode()
+
+    def set_trace(self, buf_tensor=None):
+        if buf_tensor is None:
+            check(mbci_chain_set_trace(self.h, None, 0), "mbci_chain_set_trace")
+        else:
+            check(mbci_chain_set_trace(self.h, buf_tensor.data_ptr(), buf_tensor.numel() * buf_tensor.element_size()),
+                  "mbci_chain_set_trace")
 
     def launches_per_run(self) -> int:
         return int(mbci_chain_launches_per_run(self.h))

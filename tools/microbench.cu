@@ -1,0 +1,83 @@
+// Microbenchmarks of the SIMT units the softmax step leans on (sm_100a):
+// ex2.approx.f32 / .f16x2 / .bf16x2 throughput, FFMA throughput, 3-input max.
+#include <cstdio>
+#include <cuda_fp16.h>
+#include <cuda_bf16.h>
+#define ITERS 4096
+__global__ void k_ex2_f32(float* out, float seed) {
+  float x[8];
+  for (int i = 0; i < 8; ++i) x[i] = seed * (threadIdx.x + i) * 1e-6f;
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(x[i]));
+  }
+  float s = 0; for (int i = 0; i < 8; ++i) s += x[i];
+  if (s == 12345.f) out[0] = s;
+}
+__global__ void k_ex2_f16x2(float* out, float seed) {
+  unsigned x[8];
+  for (int i = 0; i < 8; ++i) { __half2 h = __floats2half2_rn(seed * i * 1e-3f, -seed * i * 1e-3f); x[i] = *(unsigned*)&h; }
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) asm volatile("ex2.approx.f16x2 %0, %0;" : "+r"(x[i]));
+  }
+  unsigned s = 0; for (int i = 0; i < 8; ++i) s ^= x[i];
+  if (s == 12345u) out[0] = s;
+}
+__global__ void k_ex2_bf16x2(float* out, float seed) {
+  unsigned x[8];
+  for (int i = 0; i < 8; ++i) { __nv_bfloat162 h = __floats2bfloat162_rn(seed * i * 1e-3f, -seed * i * 1e-3f); x[i] = *(unsigned*)&h; }
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) asm volatile("ex2.approx.ftz.bf16x2 %0, %0;" : "+r"(x[i]));
+  }
+  unsigned s = 0; for (int i = 0; i < 8; ++i) s ^= x[i];
+  if (s == 12345u) out[0] = s;
+}
+__global__ void k_ffma(float* out, float seed) {
+  float x[8];
+  for (int i = 0; i < 8; ++i) x[i] = seed * (threadIdx.x + i);
+  const float a = 0.999f, b = 1e-7f;
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = fmaf(x[i], a, b);
+  }
+  float s = 0; for (int i = 0; i < 8; ++i) s += x[i];
+  if (s == 12345.f) out[0] = s;
+}
+__global__ void k_max3(float* out, float seed) {
+  float x[8];
+  for (int i = 0; i < 8; ++i) x[i] = seed * (threadIdx.x + i);
+  float y = seed;
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) asm volatile("max.f32 %0, %0, %1, %2;" : "+f"(x[i]) : "f"(y), "f"(x[(i+1)&7]));
+  }
+  float s = 0; for (int i = 0; i < 8; ++i) s += x[i];
+  if (s == 12345.f) out[0] = s;
+}
+typedef void (*K)(float*, float);
+int main() {
+  float* d; cudaMalloc(&d, 16);
+  int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  int clk; cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+  struct { const char* n; K k; double per; } ks[] = {
+    {"ex2.approx.ftz.f32", k_ex2_f32, 1}, {"ex2.approx.f16x2 (results)", k_ex2_f16x2, 2},
+    {"ex2.approx.ftz.bf16x2 (results)", k_ex2_bf16x2, 2}, {"ffma", k_ffma, 1}, {"max.f32 3-input", k_max3, 1}};
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  for (auto& kk : ks) {
+    for (int threads : {128, 256, 512, 1024}) {
+      kk.k<<<sms, threads>>>(d, 1.0f);
+      cudaEventRecord(e0);
+      kk.k<<<sms, threads>>>(d, 1.0f);
+      cudaEventRecord(e1); cudaEventSynchronize(e1);
+      float ms; cudaEventElapsedTime(&ms, e0, e1);
+      double ops = (double)sms * threads * ITERS * 8 * kk.per;
+      // per-SM per-clock at the max clock (clk in kHz)
+      double per_clk = ops / (ms * 1e-3) / sms / (clk * 1e3);
+      printf("%-34s threads/SM=%4d  %.3f ms  %.1f results/clk/SM (at %d MHz nominal)  err=%s\n", kk.n, threads, ms,
+             per_clk, clk / 1000, cudaGetErrorString(cudaGetLastError()));
+    }
+  }
+  return 0;
+}
