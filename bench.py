@@ -237,7 +237,10 @@ def run_cuda(args, rank, world, local_rank):
     if args.plan:
         forced = mbci.mbci_plan_t()
         forced.kernel = 0
-        forced.BN, forced.TL, forced.stages = (int(x) for x in args.plan.split(":"))
+        parts = [int(x) for x in args.plan.split(":")]
+        if len(parts) == 3:
+            parts = [0] + parts
+        forced.kernel, forced.BN, forced.TL, forced.stages = parts
     ch = mbci.Chain(nb, M, N, K, L, dtype, op, sc, b_layout=b_layout, device=local_rank, tune=args.tune,
                     plan=forced)
     plan = ch.plan()

@@ -136,9 +136,9 @@ mbci_status_t mbci_chain_plan(mbci_chain_t h, mbci_plan_t* out);
 /* Human-readable plan description into buf (NUL-terminated, truncated to len). */
 mbci_status_t mbci_chain_describe(mbci_chain_t h, char* buf, size_t len);
 
-/* Debug tracing (tensor-core path): when buf (DEVICE, >= n_block * 512 bytes) is non-NULL,
- * every later run writes 64 uint64 per CTA: %globaltimer ns at start / setup / per n-tile
- * (S ready, P written) / epilogue / end, and the SM id.  NULL turns tracing off.  INVALID if
+/* Debug tracing (tensor-core path): when buf (DEVICE, >= n_block * 1024 bytes) is non-NULL,
+ * every later run writes 128 uint64 per CTA: %globaltimer ns at start / setup / per n-tile
+ * pipeline events / epilogue / end, and the SM id.  NULL turns tracing off.  INVALID if
  * the buffer is too small. */
 mbci_status_t mbci_chain_set_trace(mbci_chain_t h, void* buf, int64_t cap_bytes);
 

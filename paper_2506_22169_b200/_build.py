@@ -8,8 +8,9 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmbci.so")
+LIB_TRACE = os.path.join(HERE, "libmbci_trace.so")
 SOURCES = [os.path.join(CSRC, "api.cu"), os.path.join(CSRC, "selector.cpp")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("chain_tc.cuh", "chain_simt.cuh", "ptx.cuh", "selector.h")] + [
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith((".cuh", ".h"))] + [
     os.path.join(os.path.dirname(HERE), "include", "mbci.h")]
 
 NVCC_FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
@@ -28,12 +29,23 @@ def stale() -> bool:
     return any(os.path.getmtime(p) > t for p in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if force or stale():
-        cmd = [nvcc()] + NVCC_FLAGS + (["-Xptxas", "-v"] if verbose else []) + ["-o", LIB + ".tmp"] + SOURCES
+def stale_lib(lib) -> bool:
+    if not os.path.exists(lib):
+        return True
+    t = os.path.getmtime(lib)
+    return any(os.path.getmtime(p) > t for p in DEPS)
+
+
+def build(force: bool = False, verbose: bool = False, trace: bool = False) -> str:
+    """libmbci.so (production) or, with trace=True, libmbci_trace.so (per-CTA event timestamps
+    compiled in; loaded by the binding when MBCI_LIB=trace — diagnostics only)."""
+    lib = LIB_TRACE if trace else LIB
+    if force or stale_lib(lib):
+        extra = ["-DMBCI_TRACE=1"] if trace else []
+        cmd = [nvcc()] + NVCC_FLAGS + extra + (["-Xptxas", "-v"] if verbose else []) + ["-o", lib + ".tmp"] + SOURCES
         subprocess.check_call(cmd)
-        os.replace(LIB + ".tmp", LIB)
-    return LIB
+        os.replace(lib + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":

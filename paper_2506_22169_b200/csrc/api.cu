@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -16,6 +17,8 @@
 #include "../../include/mbci.h"
 #include "chain_simt.cuh"
 #include "chain_tc.cuh"
+#include "chain_tc2.cuh"
+#include "chain_tc3.cuh"
 #include "selector.h"
 
 using namespace mbci;
@@ -103,6 +106,46 @@ TcKernel pick_tc(bool bf16, int bn, int kch, int bl, int dch) {
   return bf16 ? pick_bn<true>(bn, kch, bl, dch) : pick_bn<false>(bn, kch, bl, dch);
 }
 
+using Tc2Kernel = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, Tc2Params);
+
+template <bool BF16, int BN, int KCH, int BL>
+Tc2Kernel pick2_d(int dch) {
+  return dch == 1 ? (Tc2Kernel)k_chain_tc2<BF16, BN, KCH, BL, 1> : (Tc2Kernel)k_chain_tc2<BF16, BN, KCH, BL, 2>;
+}
+template <bool BF16, int BN, int KCH>
+Tc2Kernel pick2_bl(int bl, int dch) {
+  return bl == 0 ? pick2_d<BF16, BN, KCH, 0>(dch) : pick2_d<BF16, BN, KCH, 1>(dch);
+}
+template <bool BF16, int BN>
+Tc2Kernel pick2_kch(int kch, int bl, int dch) {
+  return kch == 1 ? pick2_bl<BF16, BN, 1>(bl, dch) : pick2_bl<BF16, BN, 2>(bl, dch);
+}
+template <bool BF16>
+Tc2Kernel pick2_bn(int bn, int kch, int bl, int dch) {
+  // the two-slot kernel keeps S double-buffered + O in 256 TMEM columns per slot: BN = 64 only
+  return bn == 64 ? pick2_kch<BF16, 64>(kch, bl, dch) : nullptr;
+}
+Tc2Kernel pick_tc2(bool bf16, int bn, int kch, int bl, int dch) {
+  return bf16 ? pick2_bn<true>(bn, kch, bl, dch) : pick2_bn<false>(bn, kch, bl, dch);
+}
+
+using Tc3Kernel = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, Tc3Params);
+template <bool BF16, int KCH, int BL>
+Tc3Kernel pick3_d(int dch) {
+  return dch == 1 ? (Tc3Kernel)k_chain_tc3<BF16, KCH, BL, 1> : (Tc3Kernel)k_chain_tc3<BF16, KCH, BL, 2>;
+}
+template <bool BF16, int KCH>
+Tc3Kernel pick3_bl(int bl, int dch) {
+  return bl == 0 ? pick3_d<BF16, KCH, 0>(dch) : pick3_d<BF16, KCH, 1>(dch);
+}
+template <bool BF16>
+Tc3Kernel pick3_kch(int kch, int bl, int dch) {
+  return kch == 1 ? pick3_bl<BF16, 1>(bl, dch) : pick3_bl<BF16, 2>(bl, dch);
+}
+Tc3Kernel pick_tc3(bool bf16, int kch, int bl, int dch) {
+  return bf16 ? pick3_kch<true>(kch, bl, dch) : pick3_kch<false>(kch, bl, dch);
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 std::once_flag g_encode_once;
 
@@ -153,6 +196,13 @@ struct mbci_chain {
   // tensor-core path
   TcKernel tc = nullptr;
   TcParams tp{};
+  Tc2Kernel tc2 = nullptr;
+  Tc2Params tp2{};
+  Tc3Kernel tc3 = nullptr;
+  Tc3Params tp3{};
+  int32_t grid2 = 0;
+  void* ws2 = nullptr;     // stream-K partials + flags (kernel 2)
+  size_t ws2_bytes = 0;
   int32_t kch = 1, dch = 1;
   MapCacheEntry cache[8];
   uint64_t stamp = 0;
@@ -206,6 +256,131 @@ mbci_status_t setup_plan(mbci_chain* h) {
     cudaError_t e = cudaFuncSetAttribute((const void*)h->tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          p.smem_bytes);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+  } else if (p.kernel == 2) {
+    const int32_t k_steps = static_cast<int32_t>((d.K + 15) / 16);
+    Tc2Layout lay;
+    if (!tc2_layout(k_steps, p.BN, p.TL, p.stages, d.b_layout, &lay))
+      return fail(MBCI_ERR_UNSUPPORTED, "kernel-2 plan does not fit SMEM/TMEM");
+    p.smem_bytes = lay.smem_total;
+    p.tmem_cols = 512;
+    h->kch = std::max(1, (16 * k_steps + 63) / 64);
+    h->dch = (p.TL + 63) / 64;
+    h->tc2 = pick_tc2(d.dtype == MBCI_BF16, p.BN, h->kch, d.b_layout, h->dch);
+    if (!h->tc2) return fail(MBCI_ERR_UNSUPPORTED, "kernel-2 plan needs BN = 64");
+    Tc2Params& t = h->tp2;
+    t = Tc2Params{};
+    t.M = (int32_t)d.M; t.N = (int32_t)d.N; t.K = (int32_t)d.K; t.L = (int32_t)d.L;
+    t.batch = (int32_t)d.batch;
+    t.l_m = (int32_t)((d.M + 127) / 128);
+    t.l_h = (int32_t)((d.L + p.TL - 1) / p.TL);
+    t.TL = p.TL;
+    t.k_steps = k_steps;
+    t.stages = p.stages;
+    t.a_bufs = lay.a_bufs;
+    t.op = d.op;
+    t.scale = d.op == MBCI_OP_SOFTMAX ? d.scale * 1.4426950408889634f : d.scale;
+    t.ld_e = d.ld_e;
+    t.bs_e = d.bs_e;
+    t.a_bytes = (uint32_t)lay.a_bytes;
+    t.b_stage_bytes = (uint32_t)lay.b_stage;
+    t.d_stage_bytes = (uint32_t)lay.d_stage;
+    t.kp_rows = (uint32_t)(16 * k_steps);
+    t.slot_bytes = (uint32_t)lay.slot_bytes;
+    const uint32_t fmt = d.dtype == MBCI_BF16 ? 1u : 0u;
+    t.idesc1 = ptx::idesc_f16(fmt, 0, d.b_layout == 0 ? 1u : 0u, 128, (uint32_t)p.BN);
+    t.idesc2 = ptx::idesc_f16(fmt, 0, 1u, 128, (uint32_t)p.TL);
+    t.tpu = (int32_t)std::max<int64_t>(1, (d.N + p.BN - 1) / p.BN);
+    const int64_t units = (int64_t)d.batch * t.l_m * t.l_h;
+    if (units * t.tpu > INT32_MAX) return fail(MBCI_ERR_UNSUPPORTED, "kernel-2 tile count exceeds int32");
+    t.W = (int32_t)(units * t.tpu);
+    int n_sm = 148;
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, h->device);
+    const char* one = getenv("MBCI_DEBUG_ONE_SLOT");
+    t.slots_per_cta = (one && one[0] == '1') ? 1 : 2;
+    h->grid2 = (int32_t)std::max<int64_t>(1, std::min<int64_t>(n_sm, (t.W + t.slots_per_cta - 1) / t.slots_per_cta));
+    t.n_slots = t.slots_per_cta * h->grid2;
+    p.n_block = units;
+    cudaError_t e = cudaFuncSetAttribute((const void*)h->tc2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         p.smem_bytes);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+    int occ = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)h->tc2, kT2Threads, p.smem_bytes);
+    if (e != cudaSuccess) return cuda_fail(e, "occupancy query");
+    if (occ < 1) return fail(MBCI_ERR_UNSUPPORTED, "kernel-2 CTA does not fit on an SM");
+    // workspace: partial O [P][128][TL] fp32 + (m, l) [P][2][128] + flags [P]
+    const size_t ws_floats = (size_t)t.n_slots * 128 * p.TL + (size_t)t.n_slots * 256;
+    const size_t need = ws_floats * 4 + (size_t)t.n_slots * 4;
+    if (h->ws2_bytes < need) {
+      if (h->ws2) cudaFree(h->ws2);
+      h->ws2 = nullptr;
+      h->ws2_bytes = 0;
+      if (cudaMalloc(&h->ws2, need) != cudaSuccess) return fail(MBCI_ERR_NOMEM, "stream-K workspace");
+      h->ws2_bytes = need;
+    }
+    e = cudaMemset(h->ws2, 0, need);
+    if (e != cudaSuccess) return cuda_fail(e, "workspace memset");
+    t.ws = static_cast<float*>(h->ws2);
+    t.flags = reinterpret_cast<int32_t*>(static_cast<float*>(h->ws2) + ws_floats);
+  } else if (p.kernel == 3) {
+    const int32_t k_steps = static_cast<int32_t>((d.K + 15) / 16);
+    Tc3Layout lay;
+    if (!tc3_layout(k_steps, p.TL, p.stages, d.b_layout, &lay))
+      return fail(MBCI_ERR_UNSUPPORTED, "kernel-3 plan does not fit SMEM/TMEM");
+    p.smem_bytes = lay.smem_total;
+    p.tmem_cols = 512;
+    h->kch = std::max(1, (16 * k_steps + 63) / 64);
+    h->dch = (p.TL + 63) / 64;
+    h->tc3 = pick_tc3(d.dtype == MBCI_BF16, h->kch, d.b_layout, h->dch);
+    Tc3Params& t = h->tp3;
+    t = Tc3Params{};
+    t.M = (int32_t)d.M; t.N = (int32_t)d.N; t.K = (int32_t)d.K; t.L = (int32_t)d.L;
+    t.batch = (int32_t)d.batch;
+    t.l_mp = (int32_t)((d.M + 255) / 256);
+    t.l_h = (int32_t)((d.L + p.TL - 1) / p.TL);
+    t.TL = p.TL;
+    t.k_steps = k_steps;
+    t.stages = p.stages;
+    t.q_bufs = lay.q_bufs;
+    t.op = d.op;
+    t.scale = d.op == MBCI_OP_SOFTMAX ? d.scale * 1.4426950408889634f : d.scale;
+    t.ld_e = d.ld_e;
+    t.bs_e = d.bs_e;
+    t.q_bytes = (uint32_t)lay.q_bytes;
+    t.b_stage_bytes = (uint32_t)lay.b_stage;
+    t.d_stage_bytes = (uint32_t)lay.d_stage;
+    t.kp_rows = (uint32_t)(16 * k_steps);
+    const uint32_t fmt = d.dtype == MBCI_BF16 ? 1u : 0u;
+    t.idesc1 = ptx::idesc_f16(fmt, 0, d.b_layout == 0 ? 1u : 0u, 128, 128u);
+    t.idesc2 = ptx::idesc_f16(fmt, 0, 1u, 128, (uint32_t)p.TL);
+    t.tpu = (int32_t)std::max<int64_t>(1, (d.N + 127) / 128);
+    const int64_t units = (int64_t)d.batch * t.l_mp * t.l_h;
+    if (units * t.tpu > INT32_MAX) return fail(MBCI_ERR_UNSUPPORTED, "kernel-3 tile count exceeds int32");
+    t.W = (int32_t)(units * t.tpu);
+    int n_sm = 148;
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, h->device);
+    h->grid2 = (int32_t)std::max<int64_t>(1, std::min<int64_t>(n_sm, t.W));
+    t.n_ctas = h->grid2;
+    p.n_block = units;
+    cudaError_t e = cudaFuncSetAttribute((const void*)h->tc3, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         p.smem_bytes);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+    int occ = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)h->tc3, kT3Threads, p.smem_bytes);
+    if (e != cudaSuccess) return cuda_fail(e, "occupancy query");
+    if (occ < 1) return fail(MBCI_ERR_UNSUPPORTED, "kernel-3 CTA does not fit on an SM");
+    const size_t ws_floats = (size_t)t.n_ctas * 256 * p.TL + (size_t)t.n_ctas * 512;
+    const size_t need = ws_floats * 4 + (size_t)t.n_ctas * 4;
+    if (h->ws2_bytes < need) {
+      if (h->ws2) cudaFree(h->ws2);
+      h->ws2 = nullptr;
+      h->ws2_bytes = 0;
+      if (cudaMalloc(&h->ws2, need) != cudaSuccess) return fail(MBCI_ERR_NOMEM, "stream-K workspace");
+      h->ws2_bytes = need;
+    }
+    e = cudaMemset(h->ws2, 0, need);
+    if (e != cudaSuccess) return cuda_fail(e, "workspace memset");
+    t.ws = static_cast<float*>(h->ws2);
+    t.flags = reinterpret_cast<int32_t*>(static_cast<float*>(h->ws2) + ws_floats);
   } else {
     p.n_block = d.batch * d.M;
     const void* fn = d.dtype == MBCI_F32 ? (const void*)k_chain_simt<float>
@@ -229,7 +404,7 @@ mbci_status_t launch(mbci_chain* h, const void* A, const void* B, const void* D,
   if (d.mask == MBCI_MASK_KEY_PADDING && !valid_len)
     return fail(MBCI_ERR_INVALID, "mask KEY_PADDING needs valid_len");
   const int32_t* vl = d.mask == MBCI_MASK_KEY_PADDING ? valid_len : nullptr;
-  if (h->plan.kernel == 0) {
+  if (h->plan.kernel == 0 || h->plan.kernel == 2 || h->plan.kernel == 3) {
     if (!aligned16(E) || (d.N > 0 && !aligned16(D)) || (d.K > 0 && d.N > 0 && (!aligned16(A) || !aligned16(B))))
       return fail(MBCI_ERR_UNSUPPORTED, "tensor-core path needs 16-byte aligned A, B, D, E");
     // tensor maps (cached by pointer triple)
@@ -246,17 +421,19 @@ mbci_status_t launch(mbci_chain* h, const void* A, const void* B, const void* D,
       memset(&ent->ta, 0, sizeof(CUtensorMap));
       memset(&ent->tb, 0, sizeof(CUtensorMap));
       memset(&ent->td, 0, sizeof(CUtensorMap));
+      const uint32_t bn_box = h->plan.kernel == 3 ? 128u : (uint32_t)h->plan.BN;
       if (d.K > 0 && d.N > 0) {
         s = encode3d(&ent->ta, A, bf16, d.K, d.M, d.batch, d.ld_a, d.bs_a, 128);
         if (s != MBCI_OK) return s;
+        const uint32_t kp_rows = (uint32_t)(16 * ((d.K + 15) / 16));
         if (d.b_layout == 1)
-          s = encode3d(&ent->tb, B, bf16, d.K, d.N, d.batch, d.ld_b, d.bs_b, (uint32_t)h->plan.BN);
+          s = encode3d(&ent->tb, B, bf16, d.K, d.N, d.batch, d.ld_b, d.bs_b, bn_box);
         else
-          s = encode3d(&ent->tb, B, bf16, d.N, d.K, d.batch, d.ld_b, d.bs_b, h->tp.kp_rows);
+          s = encode3d(&ent->tb, B, bf16, d.N, d.K, d.batch, d.ld_b, d.bs_b, kp_rows);
         if (s != MBCI_OK) return s;
       }
       if (d.N > 0) {
-        s = encode3d(&ent->td, D, bf16, d.L, d.N, d.batch, d.ld_d, d.bs_d, (uint32_t)h->plan.BN);
+        s = encode3d(&ent->td, D, bf16, d.L, d.N, d.batch, d.ld_d, d.bs_d, bn_box);
         if (s != MBCI_OK) return s;
       }
       ent->A = A;
@@ -264,11 +441,47 @@ mbci_status_t launch(mbci_chain* h, const void* A, const void* B, const void* D,
       ent->D = D;
     }
     ent->stamp = ++h->stamp;
-    TcParams t = h->tp;
-    t.valid_len = vl;
-    t.E = E;
-    t.trace = h->trace;
-    h->tc<<<(unsigned)h->plan.n_block, kThreads, h->plan.smem_bytes, st>>>(ent->ta, ent->tb, ent->td, t);
+    if (h->plan.kernel == 0) {
+      TcParams t = h->tp;
+      t.valid_len = vl;
+      t.E = E;
+      t.trace = h->trace;
+      h->tc<<<(unsigned)h->plan.n_block, kThreads, h->plan.smem_bytes, st>>>(ent->ta, ent->tb, ent->td, t);
+    } else if (h->plan.kernel == 3) {
+      Tc3Params t = h->tp3;
+      t.valid_len = vl;
+      t.E = E;
+      t.trace = h->trace;
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3((unsigned)h->grid2);
+      cfg.blockDim = dim3(kT3Threads);
+      cfg.dynamicSmemBytes = (size_t)h->plan.smem_bytes;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeCooperative;   // co-residency: stream-K finishers wait on peers
+      attr[0].val.cooperative = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      cudaError_t le = cudaLaunchKernelEx(&cfg, h->tc3, ent->ta, ent->tb, ent->td, t);
+      if (le != cudaSuccess) return cuda_fail(le, "cooperative launch");
+    } else {
+      Tc2Params t = h->tp2;
+      t.valid_len = vl;
+      t.E = E;
+      t.trace = h->trace;
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3((unsigned)h->grid2);
+      cfg.blockDim = dim3(kT2Threads);
+      cfg.dynamicSmemBytes = (size_t)h->plan.smem_bytes;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeCooperative;   // co-residency: stream-K finishers wait on peers
+      attr[0].val.cooperative = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      cudaError_t le = cudaLaunchKernelEx(&cfg, h->tc2, ent->ta, ent->tb, ent->td, t);
+      if (le != cudaSuccess) return cuda_fail(le, "cooperative launch");
+    }
   } else {
     SimtParams sp{};
     sp.M = (int32_t)d.M;
@@ -423,7 +636,29 @@ mbci_status_t create_impl(const mbci_chain_desc_t* desc, int device, const mbci_
     }
   }
   s = setup_plan(h);
-  if (s == MBCI_OK && !forced && d.tune == 1 && plans.size() > 1) s = tune_plan(h, plans);
+  if (s == MBCI_OK && !forced && d.tune == 1 && plans.size() > 1) {
+    // PAPER.md Alg. 1 lines 5-8: estimate every candidate, measure the top n = 8.
+    // The shortlist keeps the best-ranked plans of every kernel family so that a model error
+    // between families cannot hide the fastest kernel.
+    std::vector<mbci_plan_t> shortlist;
+    for (int fam : {0, 2, 3, 1}) {
+      int taken = 0;
+      for (const auto& q : plans)
+        if (q.kernel == fam && taken < 3) {
+          shortlist.push_back(q);
+          ++taken;
+        }
+    }
+    for (const auto& q : plans) {
+      if ((int)shortlist.size() >= 8) break;
+      bool dup = false;
+      for (const auto& r : shortlist)
+        dup |= (r.kernel == q.kernel && r.BN == q.BN && r.TL == q.TL && r.stages == q.stages);
+      if (!dup) shortlist.push_back(q);
+    }
+    if (shortlist.size() > 8) shortlist.resize(8);
+    s = tune_plan(h, shortlist);
+  }
   if (s != MBCI_OK) {
     delete h;
     return s;
@@ -507,6 +742,7 @@ mbci_status_t mbci_chain_run_host(mbci_chain_t h, const void* A, const void* B, 
 
 mbci_status_t mbci_chain_destroy(mbci_chain_t h) {
   if (!h) return MBCI_OK;
+  cudaFree(h->ws2);
   cudaFree(h->dA);
   cudaFree(h->dB);
   cudaFree(h->dD);
@@ -528,15 +764,17 @@ mbci_status_t mbci_chain_describe(mbci_chain_t h, char* buf, size_t len) {
   snprintf(buf, len,
            "kernel=%s BM=%d BN=%d TK=%d TL=%d stages=%d smem=%d tmem=%d n_block=%lld "
            "t_estm=%.3gs alpha=%.4f t_b200=%.3gs",
-           p.kernel == 0 ? "tcgen05" : "simt", p.BM, p.BN, p.TK, p.TL, p.stages, p.smem_bytes, p.tmem_cols,
+           p.kernel == 0 ? "tcgen05" : (p.kernel == 2 ? "tcgen05-streamk" : (p.kernel == 3 ? "tcgen05-pair-streamk" : "simt")), p.BM, p.BN, p.TK, p.TL, p.stages, p.smem_bytes, p.tmem_cols,
            (long long)p.n_block, p.t_estm, p.alpha, p.t_b200);
   return MBCI_OK;
 }
 
 mbci_status_t mbci_chain_set_trace(mbci_chain_t h, void* buf, int64_t cap_bytes) {
   if (!h) return fail(MBCI_ERR_INVALID, "handle is NULL");
-  if (buf && cap_bytes < h->plan.n_block * 64 * 8)
-    return fail(MBCI_ERR_INVALID, "trace buffer needs %lld bytes", (long long)(h->plan.n_block * 64 * 8));
+  const int64_t need = h->plan.kernel == 2   ? (int64_t)h->tp2.n_slots * 256 * 8
+                       : h->plan.kernel == 3 ? (int64_t)h->tp3.n_ctas * 256 * 8
+                                             : h->plan.n_block * kTraceSlots * 8;
+  if (buf && cap_bytes < need) return fail(MBCI_ERR_INVALID, "trace buffer needs %lld bytes", (long long)need);
   h->trace = static_cast<uint64_t*>(buf);
   return MBCI_OK;
 }

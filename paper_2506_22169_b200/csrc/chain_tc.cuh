@@ -48,11 +48,15 @@ struct TcParams {
   uint64_t* trace;   // optional per-CTA event timestamps (debug; see mbci_chain_set_trace)
 };
 
-// Trace slots (64 x u64 per CTA, globaltimer ns unless noted).
+// Trace slots (kTraceSlots x u64 per CTA, globaltimer ns unless noted).
+constexpr int kTraceSlots = 128;
 enum : int {
-  kTrStart = 0, kTrSetup = 1, kTrSmid = 2, kTrTileS = 3 /* +2j */, kTrTileP = 4 /* +2j */,
-  kTrEpi = 40, kTrEnd = 41, kTrAFull = 42, kTrBFull = 43 /* +j, j < 8 */, kTrTiles = 16
+  kTrStart = 0, kTrSetup = 1, kTrSmid = 2, kTrAFull = 3, kTrEpi = 4, kTrEnd = 5,
+  kTrTile0 = 8, kTrPerTile = 7, kTrTiles = 16,
+  // per tile j at kTrTile0 + kTrPerTile * j + {0: S ready, 1: S loaded, 2: max done, 3: exp done,
+  //                                           4: P arrived, 5: G1 issued, 6: G2 issued}
 };
+#define MBCI_TR(j, k) (kTrTile0 + kTrPerTile * (j) + (k))
 
 constexpr int kRowThreads = 128;
 constexpr int kThreads = 224;
@@ -83,7 +87,7 @@ __global__ void __launch_bounds__(kThreads, BN == 64 ? 2 : 1)
 
   const int warp = threadIdx.x >> 5;
   const int unit = blockIdx.x;
-  uint64_t* tr = p.trace ? p.trace + static_cast<int64_t>(blockIdx.x) * 64 : nullptr;
+  uint64_t* tr = p.trace ? p.trace + static_cast<int64_t>(blockIdx.x) * kTraceSlots : nullptr;
   if (tr && threadIdx.x == 0) {
     tr[kTrStart] = ptx::globaltimer();
     uint32_t smid;
@@ -177,7 +181,6 @@ __global__ void __launch_bounds__(kThreads, BN == 64 ? 2 : 1)
           const int s = j % S, buf = j & 1;
           if (p.k_steps > 0) {
             ptx::mbar_wait(&b_full[s], (j / S) & 1);
-            if (tr && j < 8) tr[kTrBFull + j] = ptx::globaltimer();
             ptx::tc_fence_after();
             const uint32_t b_base = ptx::smem_u32(sB + s * p.b_stage_bytes);
             for (int ks = 0; ks < p.k_steps; ++ks) {
@@ -190,6 +193,7 @@ __global__ void __launch_bounds__(kThreads, BN == 64 ? 2 : 1)
                 bd = ptx::sdesc_sw128(b_base + ks * 2048, p.kp_rows * 128, 1024);
               ptx::mma_ss(tmem + buf * BN, ad, bd, p.idesc1, ks > 0 ? 1u : 0u);
             }
+            if (tr && j < kTrTiles) tr[MBCI_TR(j, 5)] = ptx::globaltimer();
             ptx::mma_commit(&b_empty[s]);
           }
           ptx::mma_commit(&s_full[buf]);
@@ -205,6 +209,7 @@ __global__ void __launch_bounds__(kThreads, BN == 64 ? 2 : 1)
             const uint64_t dd = ptx::sdesc_sw128(d_base + ks * 2048, BN * 128, 1024);
             ptx::mma_ts(tO, tmem + buf * BN + ks * 8, dd, p.idesc2, (i > 0 || ks > 0) ? 1u : 0u);
           }
+          if (tr && i < kTrTiles) tr[MBCI_TR(i, 6)] = ptx::globaltimer();
           ptx::mma_commit(&d_empty[s]);
           ptx::mma_commit(o_done);
           if (i == nt - 1) ptx::mma_commit(o_final);
@@ -224,7 +229,8 @@ __global__ void __launch_bounds__(kThreads, BN == 64 ? 2 : 1)
     for (int j = 0; j < nt; ++j) {
       const int buf = j & 1;
       ptx::mbar_wait(&s_full[buf], (j >> 1) & 1);
-      if (tr && threadIdx.x == 0 && j < kTrTiles) tr[kTrTileS + 2 * j] = ptx::globaltimer();
+      const bool trj = tr && threadIdx.x == 0 && j < kTrTiles;
+      if (trj) tr[MBCI_TR(j, 0)] = ptx::globaltimer();
       ptx::tc_fence_after();
       uint32_t sr[BN];
       if (p.k_steps > 0) {
@@ -238,6 +244,7 @@ __global__ void __launch_bounds__(kThreads, BN == 64 ? 2 : 1)
       float s[BN];
 #pragma unroll
       for (int c = 0; c < BN; ++c) s[c] = __uint_as_float(sr[c]);
+      if (trj) tr[MBCI_TR(j, 1)] = ptx::globaltimer_after(sr[BN - 1]);
       uint32_t pk[BN / 2];
       if (p.op == 2) {
         const int valid = n_lim - j * BN;  // >= BN for a full tile
@@ -272,6 +279,7 @@ __global__ void __launch_bounds__(kThreads, BN == 64 ? 2 : 1)
           for (int c = 0; c < BN; ++c) mx = (c < valid) ? fminf(mx, s[c]) : mx;
         }
         const float m_tile = mx * sc;
+        if (trj) tr[MBCI_TR(j, 2)] = ptx::globaltimer_after(__float_as_uint(mx));
         if (j == 0) {
           m_run = m_tile;
         } else {
@@ -311,6 +319,7 @@ __global__ void __launch_bounds__(kThreads, BN == 64 ? 2 : 1)
           pk[c] = ptx::pack2<BF16>(p0, p1);
         }
         l_run += ls;
+        if (trj) tr[MBCI_TR(j, 3)] = ptx::globaltimer_after(__float_as_uint(ls));
       } else if (p.op == 1) {
 #pragma unroll
         for (int c = 0; c < BN / 2; ++c) pk[c] = ptx::pack2<BF16>(s[2 * c] * sc, s[2 * c + 1] * sc);
@@ -323,7 +332,7 @@ __global__ void __launch_bounds__(kThreads, BN == 64 ? 2 : 1)
       ptx::tmem_wait_st();
       ptx::tc_fence_before();
       ptx::mbar_arrive(&p_full[buf]);
-      if (tr && threadIdx.x == 0 && j < kTrTiles) tr[kTrTileP + 2 * j] = ptx::globaltimer();
+      if (trj) tr[MBCI_TR(j, 4)] = ptx::globaltimer();
     }
 
     // ------------------------------------------------------------ epilogue

@@ -36,6 +36,13 @@ __device__ __forceinline__ uint64_t globaltimer() {
   return t;
 }
 
+// Timer read ordered after the computation of `dep` (trace only).
+__device__ __forceinline__ uint64_t globaltimer_after(uint32_t dep) {
+  uint64_t t;
+  asm volatile("{\n\t.reg .u32 d;\n\tmov.u32 d, %1;\n\tmov.u64 %0, %%globaltimer;\n\t}" : "=l"(t) : "r"(dep));
+  return t;
+}
+
 // ---------------------------------------------------------------- mbarrier
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
@@ -67,6 +74,30 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
   return ok != 0;
 }
 
+// Non-blocking probe: has the phase with the given parity completed?
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+// Spin (no suspension) until the phase with the given parity completes; for the single-thread
+// issuer / producer roles where wake-up latency is on the critical path.
+__device__ __forceinline__ void mbar_spin(uint64_t* bar, uint32_t parity) {
+  if (mbar_test(bar, parity)) return;
+  const uint64_t t0 = globaltimer();
+  uint32_t spins = 0;
+  while (!mbar_test(bar, parity)) {
+    if (((++spins) & 4095u) == 0 && globaltimer() - t0 > 4000000000ull) __trap();
+  }
+}
+
 // Wait for the phase with the given parity to complete.  A pipeline bug must not hang the
 // GPU: after ~4 s of waiting the kernel traps (the launch then reports an error).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
@@ -76,6 +107,40 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t spins = 0;
   while (!mbar_try_wait(addr, parity)) {
     if (((++spins) & 1023u) == 0 && globaltimer() - t0 > 4000000000ull) __trap();
+  }
+}
+
+template <uint32_t N>
+__device__ __forceinline__ void setmaxnreg_inc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
+}
+template <uint32_t N>
+__device__ __forceinline__ void setmaxnreg_dec() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
+}
+
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+__device__ __forceinline__ void st_release_gpu(int32_t* addr, int32_t v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(addr), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ int32_t ld_acquire_gpu(const int32_t* addr) {
+  int32_t v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(addr) : "memory");
+  return v;
+}
+
+// Spin until *addr == v (another CTA of the same cooperative grid publishes it).  Traps after
+// ~4 s so a scheduling bug cannot hang the GPU.
+__device__ __forceinline__ void spin_acquire_gpu(const int32_t* addr, int32_t v) {
+  if (ld_acquire_gpu(addr) == v) return;
+  const uint64_t t0 = globaltimer();
+  while (ld_acquire_gpu(addr) != v) {
+    __nanosleep(64);
+    if (globaltimer() - t0 > 4000000000ull) __trap();
   }
 }
 

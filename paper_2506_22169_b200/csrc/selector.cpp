@@ -78,6 +78,41 @@ int64_t tc_smem_bytes(int32_t k_steps, int32_t BN, int32_t TL, int32_t stages, i
          1024;  // + alignment slack for the 1024-B swizzle atoms
 }
 
+bool tc2_layout(int32_t k_steps, int32_t BN, int32_t TL, int32_t stages, int32_t b_layout, Tc2Layout* out,
+                int32_t smem_max) {
+  if (2 * BN + TL > 256) return false;  // per-slot TMEM: S double-buffered (P aliased) + O
+  int32_t a, b, d;
+  tc_smem_bytes(k_steps, BN, TL, stages, b_layout, &a, &b, &d);
+  for (int32_t a_bufs = 2; a_bufs >= 1; --a_bufs) {
+    const int32_t bars = 8 * (4 + 4 * stages + 6);
+    int32_t slot = a_bufs * a + stages * (b + d) + bars;
+    slot = (slot + 1023) & ~1023;
+    const int32_t total = 2 * slot + 1024;
+    if (total + 1024 <= smem_max) {   // 1 KB left for static shared memory
+      if (out) *out = Tc2Layout{a, b, d, a_bufs, slot, total};
+      return true;
+    }
+  }
+  return false;
+}
+
+bool tc3_layout(int32_t k_steps, int32_t TL, int32_t stages, int32_t b_layout, Tc3Layout* out,
+                int32_t smem_max) {
+  if (256 + 2 * TL > 512 || TL > 128) return false;   // TMEM: S_0, S_1 (128 each) + O_0, O_1
+  int32_t a, b, d;
+  tc_smem_bytes(k_steps, 128, TL, stages, b_layout, &a, &b, &d);
+  const int32_t q = std::max<int32_t>(a, 16384);
+  for (int32_t q_bufs = 2; q_bufs >= 1; --q_bufs) {
+    const int32_t bars = 8 * (4 + 3 * stages + 5);
+    const int32_t total = q_bufs * 2 * q + stages * (b + d) + bars + 1024;
+    if (total + 1024 <= smem_max) {
+      if (out) *out = Tc3Layout{q, b, d, q_bufs, total};
+      return true;
+    }
+  }
+  return false;
+}
+
 int32_t tmem_alloc_cols(int32_t BN, int32_t TL) {
   const int32_t need = 2 * BN + TL;
   int32_t c = 32;
@@ -115,6 +150,15 @@ static void score_b200(const mbci_chain_desc_t& d, const mbci_hw_t& hw, mbci_pla
     t_tc = b * 2.0 * d.M * d.N * (d.K + d.L) / (hw.n_sm * 256.0 * hw.clock_hz);
     t_issue = t_tc;
   }
+  if (p.kernel == 2 || p.kernel == 3) {
+    // persistent stream-K: work splits evenly over 2 x n_sm slots; one prologue, no waves
+    const double units = static_cast<double>(p.n_block);
+    const double tiles = units * static_cast<double>(nt);
+    // slots differ by at most one tile; a slot holding < 1 tile of work idles the rest
+    const double qq = std::min(2.0, 1.0 + 2.0 * hw.n_sm / std::max(1.0, tiles));
+    p.t_b200 = std::max(std::max(t_hbm, t_tc), std::max(t_sfu, t_issue)) * qq + 1.5e-6;
+    return;
+  }
   int32_t occ = 1;
   if (p.kernel == 0) {
     occ = std::max<int32_t>(1, std::min<int32_t>(hw.smem_max / std::max<int32_t>(1, p.smem_bytes),
@@ -144,6 +188,52 @@ int enumerate_plans(const mbci_chain_desc_t& d, const mbci_hw_t& hw,
         for (int32_t TL = 16; TL <= lpad; TL += 16) {
           if (apply_rule3 && d.L > 0 && rule3_reject(d.L, TL)) continue;
           if (2 * BN + TL > hw.tmem_cols) continue;  // TMEM budget
+          for (int32_t st = 2; st <= 8 && BN == 128; ++st) {
+            Tc3Layout lay3;
+            if (tc3_layout(k_steps, TL, st, d.b_layout, &lay3, hw.smem_max)) {
+              mbci_plan_t p{};
+              p.kernel = 3;
+              p.BM = 256;
+              p.BN = 128;
+              p.TK = std::max<int32_t>(16, 16 * k_steps);
+              p.TL = TL;
+              p.stages = st;
+              p.smem_bytes = lay3.smem_total;
+              p.tmem_cols = 512;
+              double t[5];
+              model_terms(d.batch, d.M, d.N, d.K, d.L, p.BM, p.BN, p.TK, p.TL, s, hw, t);
+              p.t_mem = t[0];
+              p.t_comp = t[1];
+              p.alpha = t[2];
+              p.t_estm = t[3];
+              p.n_block = static_cast<int64_t>(t[4]);
+              score_b200(d, hw, p);
+              out.push_back(p);
+            }
+          }
+          for (int32_t st = 2; st <= 8; ++st) {
+            Tc2Layout lay;
+            if (BN == 64 && tc2_layout(k_steps, BN, TL, st, d.b_layout, &lay, hw.smem_max)) {
+              mbci_plan_t p{};
+              p.kernel = 2;
+              p.BM = 128;
+              p.BN = BN;
+              p.TK = std::max<int32_t>(16, 16 * k_steps);
+              p.TL = TL;
+              p.stages = st;
+              p.smem_bytes = lay.smem_total;
+              p.tmem_cols = 512;
+              double t[5];
+              model_terms(d.batch, d.M, d.N, d.K, d.L, p.BM, p.BN, p.TK, p.TL, s, hw, t);
+              p.t_mem = t[0];
+              p.t_comp = t[1];
+              p.alpha = t[2];
+              p.t_estm = t[3];
+              p.n_block = static_cast<int64_t>(t[4]);
+              score_b200(d, hw, p);
+              out.push_back(p);
+            }
+          }
           for (int32_t st = 2; st <= 4; ++st) {
             mbci_plan_t p{};
             p.kernel = 0;

@@ -12,7 +12,7 @@ import math
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmbci.so")
+LIB_PATH = os.path.join(HERE, "libmbci_trace.so" if os.environ.get("MBCI_LIB") == "trace" else "libmbci.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "

@@ -112,12 +112,16 @@ def test_enumerated_plans_are_legal_and_scored(m, shape, b_layout):
     if any(x % 8 for x in (K, b_inner, L)):        # TMA needs 16-byte row strides
         assert [p.kernel for p in plans] == [1]
         return
+    assert {p.kernel for p in plans} <= {0, 2}
     for p in plans:
-        assert p.kernel == 0 and p.BM == 128 and p.BN in (64, 128)
+        assert p.kernel in (0, 2) and p.BM == 128 and p.BN in (64, 128)
         assert p.TL % 16 == 0 and 16 <= p.TL <= lpad
         assert p.TK == max(16, math.ceil(K / 16) * 16)
         assert p.smem_bytes <= hw.smem_max
-        assert 2 * p.BN + p.TL <= p.tmem_cols <= 512 and p.tmem_cols & (p.tmem_cols - 1) == 0
+        if p.kernel == 0:    # one CTA pipeline: S double-buffered + O
+            assert 2 * p.BN + p.TL <= p.tmem_cols <= 512 and p.tmem_cols & (p.tmem_cols - 1) == 0
+        else:                # two slots of 256 columns: S double-buffered + O each
+            assert p.tmem_cols == 512 and 2 * p.BN + p.TL <= 256
         assert 2 <= p.stages <= 4
         if rule3_ok:
             assert not model.rule3_reject(N, p.BN)
