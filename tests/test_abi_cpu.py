@@ -112,23 +112,26 @@ def test_enumerated_plans_are_legal_and_scored(m, shape, b_layout):
     if any(x % 8 for x in (K, b_inner, L)):        # TMA needs 16-byte row strides
         assert [p.kernel for p in plans] == [1]
         return
-    assert {p.kernel for p in plans} <= {0, 2}
+    assert {p.kernel for p in plans} <= {0, 2, 3}
     for p in plans:
-        assert p.kernel in (0, 2) and p.BM == 128 and p.BN in (64, 128)
+        assert p.kernel in (0, 2, 3) and p.BN in (64, 128)
+        assert p.BM == (256 if p.kernel == 3 else 128)   # kernel 3: two 128-row Q tiles per CTA
         assert p.TL % 16 == 0 and 16 <= p.TL <= lpad
         assert p.TK == max(16, math.ceil(K / 16) * 16)
         assert p.smem_bytes <= hw.smem_max
         if p.kernel == 0:    # one CTA pipeline: S double-buffered + O
             assert 2 * p.BN + p.TL <= p.tmem_cols <= 512 and p.tmem_cols & (p.tmem_cols - 1) == 0
-        else:                # two slots of 256 columns: S double-buffered + O each
+        elif p.kernel == 2:  # two slots of 256 columns: S double-buffered + O each
             assert p.tmem_cols == 512 and 2 * p.BN + p.TL <= 256
-        assert 2 <= p.stages <= 4
+        else:                # two Q tiles: S_0, S_1 (128 each) + O_0, O_1
+            assert p.tmem_cols == 512 and p.BN == 128 and 256 + 2 * p.TL <= 512
+        assert 2 <= p.stages <= (4 if p.kernel == 0 else 8)
         if rule3_ok:
             assert not model.rule3_reject(N, p.BN)
-        ref = model.chain_estimate(b, M, N, K, L, 128, p.BN, p.TK, p.TL, 2, hw.W, hw.P, hw.n_sm)
+        ref = model.chain_estimate(b, M, N, K, L, p.BM, p.BN, p.TK, p.TL, 2, hw.W, hw.P, hw.n_sm)
         assert p.t_estm == pytest.approx(ref["t_estm"], rel=1e-12)
         assert p.alpha == pytest.approx(ref["alpha"], rel=1e-12)
-        assert p.n_block == b * math.ceil(M / 128) * math.ceil(L / p.TL)
+        assert p.n_block == b * math.ceil(M / p.BM) * math.ceil(L / p.TL)
     best = m.mbci_plan_t()
     assert m.mbci_plan_select(ctypes.byref(d), ctypes.byref(hw), ctypes.byref(best)) == m.MBCI_OK
     assert best.t_b200 == plans[0].t_b200
