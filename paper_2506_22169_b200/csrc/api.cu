@@ -613,7 +613,7 @@ mbci_status_t create_impl(const mbci_chain_desc_t* desc, int device, const mbci_
     hw.smem_max = (int32_t)prop.sharedMemPerBlockOptin;
   }
   std::vector<mbci_plan_t> plans;
-  enumerate_plans(d, hw, plans);
+  enumerate_plans(d, hw, plans, /*rule3=*/forced == nullptr);
   if (plans.empty())
     return fail(MBCI_ERR_UNSUPPORTED, "no legal plan (N=%lld too large for the CUDA-core path?)", (long long)d.N);
   mbci_chain* h = new (std::nothrow) mbci_chain();

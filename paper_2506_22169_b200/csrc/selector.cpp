@@ -175,14 +175,14 @@ static void score_b200(const mbci_chain_desc_t& d, const mbci_hw_t& hw, mbci_pla
 }
 
 int enumerate_plans(const mbci_chain_desc_t& d, const mbci_hw_t& hw,
-                    std::vector<mbci_plan_t>& out) {
+                    std::vector<mbci_plan_t>& out, bool rule3) {
   out.clear();
   const int32_t s = (d.dtype == MBCI_F32) ? 4 : 2;
   if (tc_eligible(d)) {
     const int32_t k_steps = static_cast<int32_t>(cdiv(d.K, 16));
     const int32_t lpad = static_cast<int32_t>(std::max<int64_t>(16, cdiv(d.L, 16) * 16));
     for (int pass = 0; pass < 2 && out.empty(); ++pass) {
-      const bool apply_rule3 = (pass == 0);
+      const bool apply_rule3 = rule3 && (pass == 0);
       for (int32_t BN : {64, 128}) {
         if (apply_rule3 && d.N > 0 && rule3_reject(d.N, BN)) continue;
         for (int32_t TL = 16; TL <= lpad; TL += 16) {

@@ -28,8 +28,10 @@ struct Tc3Layout {
 };
 bool tc3_layout(int32_t k_steps, int32_t TL, int32_t stages, int32_t b_layout, Tc3Layout* out,
                 int32_t smem_max = 232448);
+// rule3 = false skips Rule 3 entirely: an explicitly forced plan only has to be
+// legal (SMEM / TMEM / TMA), not preferred.
 int enumerate_plans(const mbci_chain_desc_t& d, const mbci_hw_t& hw,
-                    std::vector<mbci_plan_t>& out);
+                    std::vector<mbci_plan_t>& out, bool rule3 = true);
 void hw_default(mbci_hw_t* hw);
 
 }  // namespace mbci

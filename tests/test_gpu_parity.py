@@ -168,8 +168,10 @@ def test_misaligned_pointer_rejected(mbci):
 
 
 # ------------------------------------------------------------------ strides
-def test_strided_operands(mbci):
-    """Rows padded (ld > inner) and batch strides with gaps, 16-B multiples (TMA-legal)."""
+@pytest.mark.parametrize("kernel", [0, 2, 3])
+def test_strided_operands(mbci, kernel):
+    """Rows padded (ld > inner) and batch strides with gaps, 16-B multiples (TMA-legal),
+    on every tensor-core kernel family."""
     b, M, N, K, L = 3, 200, 320, 64, 48
     inp = gen.make_chain_inputs(16, "f16", b, M, N, K, L, 1)
     def pad(x, ld, bs):
@@ -183,9 +185,11 @@ def test_strided_operands(mbci):
     A, B, D = (to_dev(pad(inp.A, ldA, bsA), "f16"), to_dev(pad(inp.B, ldB, bsB), "f16"),
                to_dev(pad(inp.D, ldD, bsD), "f16"))
     E = torch.full((b * bsE,), float("nan"), dtype=torch.float16, device="cuda")
-    ch = mbci.Chain(b, M, N, K, L, "f16", "softmax", 0.125, b_layout=1,
+    pl = mbci.mbci_plan_t()
+    pl.kernel, pl.BN, pl.TL, pl.stages = kernel, (64 if kernel == 2 else 128), 48, 2
+    ch = mbci.Chain(b, M, N, K, L, "f16", "softmax", 0.125, b_layout=1, plan=pl,
                     strides=dict(ld_a=ldA, bs_a=bsA, ld_b=ldB, bs_b=bsB, ld_d=ldD, bs_d=bsD, ld_e=ldE, bs_e=bsE))
-    assert ch.plan().kernel == 0
+    assert ch.plan().kernel == kernel
     ch.run(A, B, D, E)
     torch.cuda.synchronize()
     Ef = E.cpu().float().numpy().astype(np.float64).reshape(b, bsE)
