@@ -19,6 +19,7 @@
 #include "chain_tc.cuh"
 #include "chain_tc2.cuh"
 #include "chain_tc3.cuh"
+#include "chain_tc4.cuh"
 #include "selector.h"
 
 using namespace mbci;
@@ -146,6 +147,34 @@ Tc3Kernel pick_tc3(bool bf16, int kch, int bl, int dch) {
   return bf16 ? pick3_kch<true>(kch, bl, dch) : pick3_kch<false>(kch, bl, dch);
 }
 
+using Tc4Kernel = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, Tc4Params);
+template <bool BF16, int KCH, int BL, int DCH>
+Tc4Kernel pick4_emu(int emu) {
+  constexpr int NSB = DCH == 1 ? 3 : 2;   // three S buffers fit TMEM next to two 64-column O
+  return emu == 0 ? (Tc4Kernel)k_chain_tc4<BF16, KCH, BL, DCH, 0, NSB>
+                  : (Tc4Kernel)k_chain_tc4<BF16, KCH, BL, DCH, 3, NSB>;
+}
+template <bool BF16, int KCH, int BL>
+Tc4Kernel pick4_d(int dch, int emu) {
+  return dch == 1 ? pick4_emu<BF16, KCH, BL, 1>(emu) : pick4_emu<BF16, KCH, BL, 2>(emu);
+}
+template <bool BF16, int KCH>
+Tc4Kernel pick4_bl(int bl, int dch, int emu) {
+  return bl == 0 ? pick4_d<BF16, KCH, 0>(dch, emu) : pick4_d<BF16, KCH, 1>(dch, emu);
+}
+Tc4Kernel pick_tc4(bool bf16, int kch, int bl, int dch, int emu) {
+  if (bf16) return kch == 1 ? pick4_bl<true, 1>(bl, dch, emu) : pick4_bl<true, 2>(bl, dch, emu);
+  return kch == 1 ? pick4_bl<false, 1>(bl, dch, emu) : pick4_bl<false, 2>(bl, dch, emu);
+}
+
+// Pairs of every 8 exponential pairs evaluated by the FMA-pipe polynomial in kernel 4
+// (MBCI_T4_EMU overrides; 0 = all on the MUFU).
+int t4_emu_default() {
+  const char* e = getenv("MBCI_T4_EMU");
+  if (e && (e[0] == '0' || e[0] == '3')) return e[0] - '0';
+  return 3;
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 std::once_flag g_encode_once;
 
@@ -200,6 +229,8 @@ struct mbci_chain {
   Tc2Params tp2{};
   Tc3Kernel tc3 = nullptr;
   Tc3Params tp3{};
+  Tc4Kernel tc4 = nullptr;
+  Tc4Params tp4{};
   int32_t grid2 = 0;
   void* ws2 = nullptr;     // stream-K partials + flags (kernel 2)
   size_t ws2_bytes = 0;
@@ -321,6 +352,50 @@ mbci_status_t setup_plan(mbci_chain* h) {
     if (e != cudaSuccess) return cuda_fail(e, "workspace memset");
     t.ws = static_cast<float*>(h->ws2);
     t.flags = reinterpret_cast<int32_t*>(static_cast<float*>(h->ws2) + ws_floats);
+  } else if (p.kernel == 4) {
+    const int32_t k_steps = static_cast<int32_t>((d.K + 15) / 16);
+    Tc4Layout lay;
+    if (d.op != MBCI_OP_SOFTMAX || k_steps < 1 || d.N < 1 || !tc4_layout(k_steps, p.TL, p.stages, d.b_layout, &lay))
+      return fail(MBCI_ERR_UNSUPPORTED, "kernel-4 plan needs softmax, K, N >= 1 and must fit SMEM/TMEM");
+    p.smem_bytes = lay.smem_total;
+    p.tmem_cols = 512;
+    h->kch = std::max(1, (16 * k_steps + 63) / 64);
+    h->dch = (p.TL + 63) / 64;
+    h->tc4 = pick_tc4(d.dtype == MBCI_BF16, h->kch, d.b_layout, h->dch, t4_emu_default());
+    Tc4Params& t = h->tp4;
+    t = Tc4Params{};
+    t.M = (int32_t)d.M; t.N = (int32_t)d.N; t.K = (int32_t)d.K; t.L = (int32_t)d.L;
+    t.batch = (int32_t)d.batch;
+    t.l_mp = (int32_t)((d.M + 255) / 256);
+    const int64_t units = (int64_t)d.batch * t.l_mp;
+    if (units > INT32_MAX) return fail(MBCI_ERR_UNSUPPORTED, "kernel-4 unit count exceeds int32");
+    t.units = (int32_t)units;
+    t.TL = p.TL;
+    t.k_steps = k_steps;
+    t.stages = p.stages;
+    t.q_bufs = lay.q_bufs;
+    t.scale = d.scale * 1.4426950408889634f;
+    t.ld_e = d.ld_e;
+    t.bs_e = d.bs_e;
+    if (const char* dbg = getenv("MBCI_T4_DEBUG")) t.dbg = atoi(dbg);
+    t.q_bytes = (uint32_t)lay.q_bytes;
+    t.b_stage_bytes = (uint32_t)lay.b_stage;
+    t.d_stage_bytes = (uint32_t)lay.d_stage;
+    t.kp_rows = (uint32_t)(16 * k_steps);
+    const uint32_t fmt = d.dtype == MBCI_BF16 ? 1u : 0u;
+    t.idesc1 = ptx::idesc_f16(fmt, 0, d.b_layout == 0 ? 1u : 0u, 128, 128u);
+    t.idesc2 = ptx::idesc_f16(fmt, 0, 1u, 128, (uint32_t)p.TL);
+    int n_sm = 148;
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, h->device);
+    h->grid2 = (int32_t)std::max<int64_t>(1, std::min<int64_t>(n_sm, units));
+    p.n_block = units;
+    cudaError_t e = cudaFuncSetAttribute((const void*)h->tc4, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         p.smem_bytes);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+    int occ = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)h->tc4, kT4Threads, p.smem_bytes);
+    if (e != cudaSuccess) return cuda_fail(e, "occupancy query");
+    if (occ < 1) return fail(MBCI_ERR_UNSUPPORTED, "kernel-4 CTA does not fit on an SM");
   } else if (p.kernel == 3) {
     const int32_t k_steps = static_cast<int32_t>((d.K + 15) / 16);
     Tc3Layout lay;
@@ -404,7 +479,7 @@ mbci_status_t launch(mbci_chain* h, const void* A, const void* B, const void* D,
   if (d.mask == MBCI_MASK_KEY_PADDING && !valid_len)
     return fail(MBCI_ERR_INVALID, "mask KEY_PADDING needs valid_len");
   const int32_t* vl = d.mask == MBCI_MASK_KEY_PADDING ? valid_len : nullptr;
-  if (h->plan.kernel == 0 || h->plan.kernel == 2 || h->plan.kernel == 3) {
+  if (h->plan.kernel == 0 || h->plan.kernel == 2 || h->plan.kernel == 3 || h->plan.kernel == 4) {
     if (!aligned16(E) || (d.N > 0 && !aligned16(D)) || (d.K > 0 && d.N > 0 && (!aligned16(A) || !aligned16(B))))
       return fail(MBCI_ERR_UNSUPPORTED, "tensor-core path needs 16-byte aligned A, B, D, E");
     // tensor maps (cached by pointer triple)
@@ -421,7 +496,7 @@ mbci_status_t launch(mbci_chain* h, const void* A, const void* B, const void* D,
       memset(&ent->ta, 0, sizeof(CUtensorMap));
       memset(&ent->tb, 0, sizeof(CUtensorMap));
       memset(&ent->td, 0, sizeof(CUtensorMap));
-      const uint32_t bn_box = h->plan.kernel == 3 ? 128u : (uint32_t)h->plan.BN;
+      const uint32_t bn_box = (h->plan.kernel == 3 || h->plan.kernel == 4) ? 128u : (uint32_t)h->plan.BN;
       if (d.K > 0 && d.N > 0) {
         s = encode3d(&ent->ta, A, bf16, d.K, d.M, d.batch, d.ld_a, d.bs_a, 128);
         if (s != MBCI_OK) return s;
@@ -447,6 +522,12 @@ mbci_status_t launch(mbci_chain* h, const void* A, const void* B, const void* D,
       t.E = E;
       t.trace = h->trace;
       h->tc<<<(unsigned)h->plan.n_block, kThreads, h->plan.smem_bytes, st>>>(ent->ta, ent->tb, ent->td, t);
+    } else if (h->plan.kernel == 4) {
+      Tc4Params t = h->tp4;
+      t.valid_len = vl;
+      t.E = E;
+      t.trace = h->trace;
+      h->tc4<<<(unsigned)h->grid2, kT4Threads, h->plan.smem_bytes, st>>>(ent->ta, ent->tb, ent->td, t);
     } else if (h->plan.kernel == 3) {
       Tc3Params t = h->tp3;
       t.valid_len = vl;
@@ -641,7 +722,7 @@ mbci_status_t create_impl(const mbci_chain_desc_t* desc, int device, const mbci_
     // The shortlist keeps the best-ranked plans of every kernel family so that a model error
     // between families cannot hide the fastest kernel.
     std::vector<mbci_plan_t> shortlist;
-    for (int fam : {0, 2, 3, 1}) {
+    for (int fam : {4, 0, 2, 3, 1}) {
       int taken = 0;
       for (const auto& q : plans)
         if (q.kernel == fam && taken < 3) {
@@ -764,7 +845,7 @@ mbci_status_t mbci_chain_describe(mbci_chain_t h, char* buf, size_t len) {
   snprintf(buf, len,
            "kernel=%s BM=%d BN=%d TK=%d TL=%d stages=%d smem=%d tmem=%d n_block=%lld "
            "t_estm=%.3gs alpha=%.4f t_b200=%.3gs",
-           p.kernel == 0 ? "tcgen05" : (p.kernel == 2 ? "tcgen05-streamk" : (p.kernel == 3 ? "tcgen05-pair-streamk" : "simt")), p.BM, p.BN, p.TK, p.TL, p.stages, p.smem_bytes, p.tmem_cols,
+           p.kernel == 0 ? "tcgen05" : (p.kernel == 2 ? "tcgen05-streamk" : (p.kernel == 3 ? "tcgen05-pair-streamk" : (p.kernel == 4 ? "tcgen05-pingpong" : "simt"))), p.BM, p.BN, p.TK, p.TL, p.stages, p.smem_bytes, p.tmem_cols,
            (long long)p.n_block, p.t_estm, p.alpha, p.t_b200);
   return MBCI_OK;
 }
@@ -773,6 +854,7 @@ mbci_status_t mbci_chain_set_trace(mbci_chain_t h, void* buf, int64_t cap_bytes)
   if (!h) return fail(MBCI_ERR_INVALID, "handle is NULL");
   const int64_t need = h->plan.kernel == 2   ? (int64_t)h->tp2.n_slots * 256 * 8
                        : h->plan.kernel == 3 ? (int64_t)h->tp3.n_ctas * 256 * 8
+                       : h->plan.kernel == 4 ? (int64_t)h->grid2 * kT4TraceSlots * 8
                                              : h->plan.n_block * kTraceSlots * 8;
   if (buf && cap_bytes < need) return fail(MBCI_ERR_INVALID, "trace buffer needs %lld bytes", (long long)need);
   h->trace = static_cast<uint64_t*>(buf);

@@ -1,0 +1,600 @@
+// chain_tc4.cuh — persistent ping-pong attention chain E = softmax(s·A·B)·D on sm_100a.
+//
+// Same arithmetic as chain_tc.cuh for op = SOFTMAX (mbci.h; PAPER.md:196 chain, :498 softmax
+// between the GEMMs, :489 batched layout); a different layout of the work, built for the MUFU
+// (ex2) + tensor-core balance of d <= 128 attention on B200:
+//
+// * Persistent grid (one CTA per SM).  A unit is (β, a PAIR of 128-row m-tiles) — the paper's
+//   spatial loop m bound to CTAs (Rule 1) with the whole L in the CTA (the h loop
+//   is dead for L <= 128) — and units are dealt round-robin to CTAs.  K = A's width <= 128 makes
+//   the k loop dead, so both Q tiles of a unit are loaded once and E is stored
+//   once per unit after the n loop (S_E hoisted).
+// * Each K_j / V_j tile (B_j, D_j) is loaded once and feeds both Q tiles ("slots").  The two
+//   softmax warpgroups work on the two slots; the single tcgen05 issuer interleaves the slots,
+//   so while one slot's warpgroup computes exponentials the tensor core serves the other.
+//   The look-ahead G1s cross unit boundaries: the next unit's first S tiles are computed while
+//   the current unit's last P is still being produced (Q is double-buffered when SMEM allows).
+// * A separate epilogue warpgroup drains O (E = O / l, cvt, store), so the softmax warpgroups
+//   start the next unit at once; O_x is released to the next unit's first G2 by `o_free`.
+// * TMEM (512 columns): NSB fp32 S buffers of 128 columns rotated over the slot-tile sequence,
+//   then O_0, O_1 (see NSB below).  P (16-bit, two per column) overwrites the first 64 columns
+//   of the S buffer it came from.  tcgen05 ops of one thread complete in issue order, so a G1
+//   rewrites a buffer only after the G2 that read its P.
+// * Exponentials: z = s·log2(e)·S − m with packed f32x2 FMA; p = 2^z on the MUFU (ex2.approx)
+//   or, for EMU of every 8 column pairs, on the FMA pipe (Cody–Waite split + degree-3 minimax
+//   polynomial, max rel. error 8.8e-5 < the 16-bit P rounding) so both pipes share the work.
+//   Lazy rescale: the running max only moves when a tile's max exceeds it by > τ = 8 (log2),
+//   exact in real arithmetic (R4).
+//
+// Warps: 0-3 softmax slot 0 | 4-7 softmax slot 1 | 8-11 epilogue | 12 tcgen05 issuer + TMEM
+//        allocator | 13 TMA producer | 14-15 idle.  Every role fits in the 128 registers of a
+//        512-thread CTA (the softmax streams S through registers 32-64 columns at a time).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cstdint>
+
+#include "ptx.cuh"
+
+#ifndef MBCI_TRACE
+#define MBCI_TRACE 0
+#endif
+
+namespace mbci {
+
+struct Tc4Params {
+  int32_t M, N, K, L;
+  int32_t batch, l_mp;     // 256-row pair units per β
+  int32_t units;           // batch * l_mp
+  int32_t TL;              // L padded to 16 (<= 128): O columns per slot
+  int32_t k_steps;         // ceil(K / 16) >= 1
+  int32_t stages;          // K/V ring depth
+  int32_t q_bufs;          // Q-pair buffers (1 or 2)
+  float scale;             // softmax scale * log2(e)
+  const int32_t* valid_len;
+  void* E;
+  int64_t ld_e, bs_e;
+  uint32_t q_bytes;        // one 128-row Q tile
+  uint32_t b_stage_bytes, d_stage_bytes, kp_rows;
+  uint32_t idesc1, idesc2;
+  uint64_t* trace;         // [gridDim.x][kT4TraceSlots] (MBCI_TRACE builds only)
+  int32_t dbg;             // diagnostics only (MBCI_T4_DEBUG): 1 = softmax skips its TMEM/math work,
+                           // 2 = issuer skips the G2 MMAs, 4 = issuer skips the G1 MMAs
+};
+
+constexpr int kT4Threads = 512;
+constexpr int kT4BN = 128;
+constexpr float kT4Tau = 8.0f;
+constexpr int kT4TraceSlots = 512;
+// trace layout per CTA (MBCI_TRACE builds): [0] start (globaltimer ns) [1] setup [2] smid [3] end,
+// [4] clock64 at start; per flat tile g < 40 and slot x, SM clock64 at 8 + 12*g + {0+x: S ready,
+// 2+x: tile max done, 4+x: P stored, 6+x: P seen by the issuer, 8+x: G2 issued, 10+x: G1(g+1)
+// issued, 12: issuer starts waiting for K_g, 13: K_g landed, 14+x: issuer starts waiting for P};
+// [460 + g] TMA issues the K/V load of tile g; per unit u < 4 at 490 + 4*u + {0: o_full seen, 1: slot 0 stored, 2: slot 1 stored}.
+#define T4TR(g, k) (8 + 16 * (g) + (k))
+constexpr int kT4TrTiles = 28;
+__device__ __forceinline__ uint64_t t4_clk() {
+  uint64_t c;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+  return c;
+}
+__device__ __forceinline__ uint64_t t4_clk_after(uint32_t dep) {
+  uint64_t c;
+  asm volatile("{\n\t.reg .u32 d;\n\tmov.u32 d, %1;\n\tmov.u64 %0, %%clock64;\n\t}" : "=l"(c) : "r"(dep));
+  return c;
+}
+
+__device__ __forceinline__ int t4_nlim(const Tc4Params& p, int beta) {
+  int n = p.N;
+  if (p.valid_len != nullptr) n = min(max(__ldg(p.valid_len + beta), 0), p.N);
+  return n;
+}
+
+// 2^x for a pair, on the FMA/ALU pipes.  x <= 2^22; results below 2^-127 flush towards 0.
+//   x = n + f, n = floor(x) (round-down add of 1.5·2^23), f in [0, 1);
+//   2^f ~= ((c3 f + c2) f + c1) f + c0 (minimax, relative error 8.8e-5); 2^n by exponent add.
+__device__ __forceinline__ float2 t4_exp2_poly(float2 x) {
+  constexpr float kMagic = 12582912.0f;   // 1.5 * 2^23
+  x.x = fmaxf(x.x, -127.0f);
+  x.y = fmaxf(x.y, -127.0f);
+  const float2 t = __fadd2_rd(x, make_float2(kMagic, kMagic));
+  const float2 fl = __fadd2_rn(t, make_float2(-kMagic, -kMagic));
+  const float2 f = __ffma2_rn(fl, make_float2(-1.0f, -1.0f), x);
+  float2 q = __ffma2_rn(f, make_float2(0.0771190897f, 0.0771190897f),
+                        make_float2(0.2275643945f, 0.2275643945f));
+  q = __ffma2_rn(q, f, make_float2(0.6951461434f, 0.6951461434f));
+  q = __ffma2_rn(q, f, make_float2(1.0f, 1.0f));
+  float2 r;
+  r.x = __uint_as_float(__float_as_uint(q.x) + (__float_as_uint(t.x) << 23));
+  r.y = __uint_as_float(__float_as_uint(q.y) + (__float_as_uint(t.y) << 23));
+  return r;
+}
+
+// Row extreme of a 128-column S tile in TMEM (max, or min when the scale is negative), read in
+// two 64-column halves so that no more than 64 scores are live in registers.
+template <bool MIN>
+__device__ __forceinline__ float t4_red(float a, float b, float c) {
+  return MIN ? ptx::min3(a, b, c) : ptx::max3(a, b, c);
+}
+template <bool MIN>
+__device__ __forceinline__ float t4_tile_extreme(uint32_t tS) {
+  float a0, a1, a2, a3;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    uint32_t r[64];
+    ptx::tmem_ld32(tS + h * 64, r);
+    ptx::tmem_ld32(tS + h * 64 + 32, r + 32);
+    ptx::tmem_wait_ld();
+    int c0 = 0;
+    if (h == 0) {
+      a0 = __uint_as_float(r[0]);
+      a1 = __uint_as_float(r[1]);
+      a2 = __uint_as_float(r[2]);
+      a3 = __uint_as_float(r[3]);
+      c0 = 4;
+    }
+#pragma unroll
+    for (int c = c0; c < 64; c += 8) {
+      a0 = t4_red<MIN>(a0, __uint_as_float(r[c]), __uint_as_float(r[c + 1]));
+      a1 = t4_red<MIN>(a1, __uint_as_float(r[c + 2]), __uint_as_float(r[c + 3]));
+      if (c + 4 < 64) {
+        a2 = t4_red<MIN>(a2, __uint_as_float(r[c + 4]), __uint_as_float(r[c + 5]));
+        a3 = t4_red<MIN>(a3, __uint_as_float(r[c + 6]), __uint_as_float(r[c + 7]));
+      }
+    }
+  }
+  return t4_red<MIN>(a0, a1, MIN ? fminf(a2, a3) : fmaxf(a2, a3));
+}
+// Same over the first `valid` (< 128) columns only: keys n >= n_lim are masked (−inf).
+template <bool MIN>
+__device__ __forceinline__ float t4_tile_extreme_masked(uint32_t tS, int valid) {
+  float mx = MIN ? INFINITY : -INFINITY;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    uint32_t r[64];
+    ptx::tmem_ld32(tS + h * 64, r);
+    ptx::tmem_ld32(tS + h * 64 + 32, r + 32);
+    ptx::tmem_wait_ld();
+#pragma unroll
+    for (int c = 0; c < 64; ++c) {
+      const float v = __uint_as_float(r[c]);
+      if (h * 64 + c < valid) mx = MIN ? fminf(mx, v) : fmaxf(mx, v);
+    }
+  }
+  return mx;
+}
+
+// p = 2^(sc·S − m) over the 128 columns of S_x, written back as 16-bit P into columns
+// [0, 64) of S_x (each 32-column S chunk becomes 16 packed columns, which only overwrite
+// S columns already read).  The next chunk's tcgen05.ld is in flight while the current one is
+// exponentiated.  MASKED: columns >= valid give p = 0.
+template <bool BF16, int EMU, bool MASKED>
+__device__ __forceinline__ void t4_exp_tile(uint32_t tS, float sc, float m, int valid, float2& l2) {
+  const float2 sc2 = make_float2(sc, sc);
+  const float2 nm2 = make_float2(-m, -m);
+  uint32_t ra[32], rb[32];
+  ptx::tmem_ld32(tS, ra);
+  ptx::tmem_wait_ld();
+#pragma unroll
+  for (int ch = 0; ch < 4; ++ch) {
+    uint32_t* cur = (ch & 1) ? rb : ra;
+    uint32_t* nxt = (ch & 1) ? ra : rb;
+    if (ch < 3) ptx::tmem_ld32(tS + (ch + 1) * 32, nxt);
+    uint32_t pk[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+      const float2 z = __ffma2_rn(make_float2(__uint_as_float(cur[2 * c]), __uint_as_float(cur[2 * c + 1])), sc2, nm2);
+      const int cp = ch * 16 + c;   // pair index in the tile
+      float2 e;
+      if (EMU > 0 && ((cp * EMU) & 7) < EMU) {
+        e = t4_exp2_poly(z);
+      } else {
+        e.x = ptx::ex2(z.x);
+        e.y = ptx::ex2(z.y);
+      }
+      if (MASKED) {
+        e.x = (2 * cp < valid) ? e.x : 0.f;
+        e.y = (2 * cp + 1 < valid) ? e.y : 0.f;
+      }
+      l2 = __fadd2_rn(l2, e);
+      pk[c] = ptx::pack2<BF16>(e.x, e.y);
+    }
+    ptx::tmem_st16(tS + ch * 16, pk);
+    if (ch < 3) ptx::tmem_wait_ld();
+  }
+}
+
+// Cursor over a CTA's flat sequence of key tiles (units dealt round-robin, units with no valid
+// key skipped): unit u, its tile count nt, tile j inside it, the unit's Q buffer (qb, parity
+// qph) and active-unit index ai, and the K/V ring stage (st, parity sph) of the tile.  Per tile
+// the issuer only increments counters; divisions happen once per unit.
+struct T4Cursor {
+  int u, nt, j, ai, qb, qph, st, sph, g;
+  bool valid;
+  __device__ __forceinline__ void skip(const Tc4Params& p, int G) {
+    while (u < p.units) {
+      nt = (t4_nlim(p, u / p.l_mp) + kT4BN - 1) / kT4BN;
+      if (nt > 0) return;
+      u += G;
+    }
+    valid = false;
+  }
+  __device__ __forceinline__ void init(const Tc4Params& p, int G) {
+    u = blockIdx.x; j = 0; ai = 0; qb = 0; qph = 0; st = 0; sph = 0; g = 0; valid = true; nt = 0;
+    skip(p, G);
+  }
+  __device__ __forceinline__ void advance(const Tc4Params& p, int G) {
+    ++g;
+    if (++st == p.stages) { st = 0; sph ^= 1; }
+    if (++j >= nt) {
+      j = 0;
+      ++ai;
+      if (++qb == p.q_bufs) { qb = 0; qph ^= 1; }
+      u += G;
+      skip(p, G);
+    }
+  }
+};
+
+// NSB: S buffers in TMEM, rotated over the flat slot-tile sequence k = 2g + x (buffer k % NSB).
+//   NSB = 2 (TL > 64): S_x is reused by slot x only, G1(k+2) follows G2(k).
+//   NSB = 3 (TL <= 64): three 128-column S buffers + two 64-column O; G1(k+3) follows G2(k), so
+//   a slot's next S tile is computed while its softmax still runs (the softmax warpgroups never
+//   wait for G2 + G1 latency), and the lazy rescale waits for G2_x(j-1) via S(k+1)'s phase.
+// Commits are the scarce resource of the issuer (tools/commit_bench.cu: each tcgen05.commit
+// occupies the tensor pipe ~220 cycles): per slot-tile one (s_full), plus o_full per unit and
+// slot and q_empty per unit; everything else is inferred from those phases.
+template <bool BF16, int KCH, int BL, int DCH, int EMU, int NSB>
+__global__ void __launch_bounds__(kT4Threads, 1)
+    k_chain_tc4(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const __grid_constant__ CUtensorMap tmD, const Tc4Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  __shared__ uint32_t tmem_base_slot;
+  __shared__ float l_sm[2][2][128];   // [slot][active-unit parity][row]
+
+  constexpr uint32_t kOCol = NSB * 128;                 // O_0 column; O_1 at kOCol + kOStride
+  constexpr uint32_t kOStride = NSB == 3 ? 64 : 128;
+  // The K/V slot of tile g is released by softmax slot kRelX on seeing S of its tile g + kRelD
+  // (slot-tile 2g + 1 + NSB): no tcgen05.commit is spent on the ring (each costs ~220 cycles of
+  // the tensor pipe, tools/commit_bench.cu).  Needs stages > kRelD.
+  constexpr int kRelX = (NSB + 1) & 1;
+  constexpr int kRelD = (NSB + 1) >> 1;
+  const int S = p.stages;
+  const uint32_t kv_stage = p.b_stage_bytes + p.d_stage_bytes;
+  uint8_t* sQ = smem;                                      // [q_bufs][2][q_bytes]
+  uint8_t* sKV = sQ + p.q_bufs * 2 * p.q_bytes;            // [S][K | V]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + S * kv_stage);
+  uint64_t* q_full = bars;          // [2]
+  uint64_t* q_empty = bars + 2;     // [2]
+  uint64_t* o_full = bars + 4;      // [2] last G2_x of a unit completed
+  uint64_t* o_free = bars + 6;      // [2] epilogue read O_x (128 arrivals)
+  uint64_t* l_full = bars + 8;      // [2] softmax x published l (128 arrivals)
+  uint64_t* l_free = bars + 10;     // [2] epilogue read l_sm[x][ai & 1] (128 arrivals)
+  uint64_t* s_full = bars + 12;     // [NSB] G1 landed in S buffer b
+  uint64_t* p_full = s_full + 3;    // [NSB] softmax wrote P into buffer b (128 arrivals)
+  uint64_t* k_full = p_full + 3;    // [S]
+  uint64_t* v_full = k_full + S;    // [S]
+  uint64_t* kv_empty = v_full + S;  // [S] both G2 of the tile completed (softmax arrival)
+
+  const int warp = threadIdx.x >> 5;
+#if MBCI_TRACE
+  uint64_t* tr = p.trace ? p.trace + static_cast<int64_t>(blockIdx.x) * kT4TraceSlots : nullptr;
+#else
+  constexpr uint64_t* tr = nullptr;
+#endif
+  if (threadIdx.x == 0) {
+    if (tr) {
+      tr[0] = ptx::globaltimer();
+      tr[4] = t4_clk();
+      uint32_t smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      tr[2] = smid;
+    }
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&q_full[i], 1);
+      ptx::mbar_init(&q_empty[i], 1);
+      ptx::mbar_init(&o_full[i], 1);
+      ptx::mbar_init(&o_free[i], 128);
+      ptx::mbar_init(&l_full[i], 128);
+      ptx::mbar_init(&l_free[i], 128);
+    }
+    for (int b = 0; b < NSB; ++b) {
+      ptx::mbar_init(&s_full[b], 1);
+      ptx::mbar_init(&p_full[b], 128);
+    }
+    for (int s = 0; s < S; ++s) {
+      ptx::mbar_init(&k_full[s], 1);
+      ptx::mbar_init(&v_full[s], 1);
+      ptx::mbar_init(&kv_empty[s], 1);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 13) {
+    ptx::tma_prefetch(&tmA);
+    ptx::tma_prefetch(&tmB);
+    ptx::tma_prefetch(&tmD);
+  }
+  if (warp == 12) ptx::tmem_alloc(&tmem_base_slot, 512);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = tmem_base_slot;
+  if (tr && threadIdx.x == 0) tr[1] = ptx::globaltimer();
+  const int G = gridDim.x;
+
+  if (warp >= 12) {
+    if (warp == 13) {
+      // ============================================================ TMA producer
+      if (ptx::elect_one()) {
+        int g = 0, ai = 0;
+        for (int u = blockIdx.x; u < p.units; u += G) {
+          const int beta = u / p.l_mp;
+          const int m0 = (u - beta * p.l_mp) * 256;
+          const int nt = (t4_nlim(p, beta) + kT4BN - 1) / kT4BN;
+          if (nt == 0) continue;
+          const int qb = ai % p.q_bufs;
+          if (ai >= p.q_bufs) ptx::mbar_wait(&q_empty[qb], ((ai / p.q_bufs) - 1) & 1);
+          const bool two = m0 + 128 < p.M;   // a fully out-of-range second tile is not loaded
+          ptx::mbar_arrive_expect_tx(&q_full[qb], (two ? 2u : 1u) * p.q_bytes);
+          for (int x = 0; x < (two ? 2 : 1); ++x) {
+            uint8_t* dst = sQ + (qb * 2 + x) * p.q_bytes;
+#pragma unroll
+            for (int c = 0; c < KCH; ++c)
+              ptx::tma_load_3d(dst + c * 16384, &tmA, &q_full[qb], c * 64, m0 + x * 128, beta);
+          }
+          ++ai;
+          for (int j = 0; j < nt; ++j, ++g) {
+            const int s = g % S;
+            if (g >= S) ptx::mbar_wait(&kv_empty[s], ((g / S) - 1) & 1);
+            uint8_t* kdst = sKV + s * kv_stage;
+            uint8_t* vdst = kdst + p.b_stage_bytes;
+            if (tr && g < kT4TrTiles) tr[460 + g] = t4_clk();   // K/V load of tile g issued
+            ptx::mbar_arrive_expect_tx(&k_full[s], p.b_stage_bytes);
+            if constexpr (BL == 1) {
+#pragma unroll
+              for (int c = 0; c < KCH; ++c)
+                ptx::tma_load_3d(kdst + c * (kT4BN * 128), &tmB, &k_full[s], c * 64, j * kT4BN, beta);
+            } else {
+#pragma unroll
+              for (int c = 0; c < kT4BN / 64; ++c)
+                ptx::tma_load_3d(kdst + c * (p.kp_rows * 128), &tmB, &k_full[s], j * kT4BN + c * 64, 0, beta);
+            }
+            ptx::mbar_arrive_expect_tx(&v_full[s], p.d_stage_bytes);
+#pragma unroll
+            for (int c = 0; c < DCH; ++c)
+              ptx::tma_load_3d(vdst + c * (kT4BN * 128), &tmD, &v_full[s], c * 64, j * kT4BN, beta);
+          }
+        }
+      }
+    } else if (warp == 12) {
+      // ============================================================ tcgen05 issuer
+      if (ptx::elect_one()) {
+        const uint64_t dA = ptx::sdesc_sw128(0, 16, 1024);
+        const uint64_t dB = (BL == 1) ? ptx::sdesc_sw128(0, 16, 1024) : ptx::sdesc_sw128(0, p.kp_rows * 128, 1024);
+        const uint64_t dD = ptx::sdesc_sw128(0, kT4BN * 128, 1024);
+        const uint32_t sQ0 = ptx::smem_u32(sQ), sKV0 = ptx::smem_u32(sKV);
+        const uint32_t idesc1 = p.idesc1, idesc2 = p.idesc2;
+        const int k_steps = p.k_steps;
+        T4Cursor c1, c2;   // c1: tile of the next G1, c2: tile of the next G2
+        c1.init(p, G);
+        c2 = c1;
+        int b1 = 0, b2 = 0, pph = 0;   // S buffer of the next G1 / G2, p_full parity of b2
+        int x1 = 0;                    // slot of the next G1
+        bool tail_committed = false;
+        // G1: S_b1 = Q_x1 · K_(c1 tile)
+        auto issue_g1 = [&]() {
+          if (!c1.valid) {
+            // past the CTA's last tile: one bare commit on the next buffer's s_full, so a lazy
+            // rescale of the last slot-tile (which waits for "G1(k + 1)") still completes
+            if (!tail_committed) ptx::mma_commit(&s_full[b1]);
+            tail_committed = true;
+            return;
+          }
+          if (x1 == 0) {
+            if (tr && c1.g < kT4TrTiles) tr[T4TR(c1.g, 12)] = t4_clk();
+            if (c1.j == 0) ptx::mbar_spin(&q_full[c1.qb], c1.qph);
+            ptx::mbar_spin(&k_full[c1.st], c1.sph);
+            if (tr && c1.g < kT4TrTiles) tr[T4TR(c1.g, 13)] = t4_clk();
+            ptx::tc_fence_after();
+          }
+          const uint32_t q_lo = (sQ0 + (c1.qb * 2 + x1) * p.q_bytes) >> 4;
+          const uint32_t k_lo = (sKV0 + c1.st * kv_stage) >> 4;
+          const uint32_t dS = tmem + b1 * 128;
+#pragma unroll
+          for (int ks = 0; ks < 4 * KCH; ++ks) {
+            if (ks < k_steps) {
+              const uint64_t ad = dA + q_lo + (ks >> 2) * 1024 + (ks & 3) * 2;
+              const uint64_t bd = (BL == 1) ? dB + k_lo + (ks >> 2) * (kT4BN * 8) + (ks & 3) * 2
+                                            : dB + k_lo + ks * 128;
+              if (!(p.dbg & 4)) ptx::mma_ss(dS, ad, bd, idesc1, ks > 0 ? 1u : 0u);
+            }
+          }
+          ptx::mma_commit(&s_full[b1]);
+          if (tr && c1.g < kT4TrTiles) tr[T4TR(c1.g, 10 + x1)] = t4_clk();
+          if (++b1 == NSB) b1 = 0;
+          if (x1 == 1) {
+            if (c1.j == c1.nt - 1) ptx::mma_commit(&q_empty[c1.qb]);
+            c1.advance(p, G);
+          }
+          x1 ^= 1;
+        };
+#pragma unroll 1
+        for (int i = 0; i < NSB; ++i) issue_g1();
+        int x2 = 0;
+        while (c2.valid) {
+          if (tr && c2.g < kT4TrTiles) tr[T4TR(c2.g, 14 + x2)] = t4_clk();
+          ptx::mbar_spin(&p_full[b2], pph);
+          if (tr && c2.g < kT4TrTiles) tr[T4TR(c2.g, 6 + x2)] = t4_clk();
+          if (c2.j == 0 && c2.ai > 0) ptx::mbar_spin(&o_free[x2], (c2.ai - 1) & 1);
+          if (x2 == 0) ptx::mbar_spin(&v_full[c2.st], c2.sph);
+          ptx::tc_fence_after();
+          // G2: O_x2 (+)= P_b2 · V_(c2 tile)
+          const uint32_t v_lo = (sKV0 + c2.st * kv_stage + p.b_stage_bytes) >> 4;
+          const uint32_t tO = tmem + kOCol + x2 * kOStride;
+          const uint32_t tP = tmem + b2 * 128;
+          const uint32_t acc0 = c2.j > 0 ? 1u : 0u;
+#pragma unroll
+          for (int ks = 0; ks < kT4BN / 16; ++ks)
+            if (!(p.dbg & 2)) ptx::mma_ts(tO, tP + ks * 8, dD + v_lo + ks * 128, idesc2, ks > 0 ? 1u : acc0);
+          if (tr && c2.g < kT4TrTiles) tr[T4TR(c2.g, 8 + x2)] = t4_clk();
+          if (c2.j == c2.nt - 1) ptx::mma_commit(&o_full[x2]);
+          if (++b2 == NSB) { b2 = 0; pph ^= 1; }
+          if (x2 == 1) c2.advance(p, G);
+          x2 ^= 1;
+          issue_g1();   // the next G1 reuses the buffer this G2 just read
+        }
+      }
+    }
+  } else if (warp >= 8) {
+    // ============================================================ epilogue (warps 8-11)
+    const int row = threadIdx.x - 256;   // TMEM lane (warp 8+w reads lanes 32w..32w+31)
+    const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    using T16 = uint16_t;
+    int ai = 0;
+    for (int u = blockIdx.x; u < p.units; u += G) {
+      const int beta = u / p.l_mp;
+      const int m0 = (u - beta * p.l_mp) * 256;
+      const int nt = (t4_nlim(p, beta) + kT4BN - 1) / kT4BN;
+#pragma unroll 1
+      for (int x = 0; x < 2; ++x) {
+        const int gm = m0 + x * 128 + row;
+        T16* erow = reinterpret_cast<T16*>(p.E) + static_cast<int64_t>(beta) * p.bs_e +
+                    static_cast<int64_t>(gm) * p.ld_e;
+        float inv = 0.f;
+        const uint32_t tO = tmem + lane_off + kOCol + x * kOStride;
+        if (nt > 0) {
+          ptx::mbar_wait(&o_full[x], ai & 1);
+          ptx::tc_fence_after();
+          if (tr && x == 0 && row == 0 && ai < 4) tr[490 + 4 * ai] = t4_clk();
+          ptx::mbar_wait(&l_full[x], ai & 1);
+          const float l = l_sm[x][ai & 1][row];
+          ptx::mbar_arrive(&l_free[x]);
+          inv = l > 0.f ? 1.0f / l : 0.f;
+        }
+#pragma unroll 1
+        for (int c0 = 0; c0 < p.TL; c0 += 16) {
+          uint32_t r[16];
+          if (nt > 0) {
+            ptx::tmem_ld16(tO + c0, r);
+            ptx::tmem_wait_ld();
+          } else {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) r[q] = 0u;
+          }
+          uint32_t w[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            w[q] = ptx::pack2<BF16>(__uint_as_float(r[2 * q]) * inv, __uint_as_float(r[2 * q + 1]) * inv);
+          if (gm < p.M) {
+            if (c0 + 16 <= p.L) {
+              uint4* dst = reinterpret_cast<uint4*>(erow + c0);
+              dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+              dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+            } else {
+#pragma unroll
+              for (int q = 0; q < 16; ++q)
+                if (c0 + q < p.L) erow[c0 + q] = static_cast<T16>((w[q >> 1] >> ((q & 1) * 16)) & 0xFFFFu);
+            }
+          }
+        }
+        if (nt > 0) {
+          ptx::tc_fence_before();
+          ptx::mbar_arrive(&o_free[x]);
+        }
+        if (tr && row == 0 && ai < 4) tr[490 + 4 * ai + 1 + x] = t4_clk();
+      }
+      if (nt > 0) ++ai;
+    }
+  } else {
+    // ============================================================ softmax (warps 0-7)
+    const int x = warp >> 2;               // slot
+    const int row = threadIdx.x & 127;     // TMEM lane
+    const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    const uint32_t tO = tmem + lane_off + kOCol + x * kOStride;
+    const float sc = p.scale;
+    int g = 0, ai = 0;
+    for (int u = blockIdx.x; u < p.units; u += G) {
+      const int beta = u / p.l_mp;
+      const int n_lim = t4_nlim(p, beta);
+      const int nt = (n_lim + kT4BN - 1) / kT4BN;
+      if (nt == 0) continue;
+      float m_run = 0.f;
+      float2 l2 = make_float2(0.f, 0.f);
+      for (int j = 0; j < nt; ++j, ++g) {
+        const int k = 2 * g + x, b = k % NSB;
+        const uint32_t tS = tmem + lane_off + b * 128;
+        ptx::mbar_wait(&s_full[b], (k / NSB) & 1);
+        ptx::tc_fence_after();
+        if (tr && row == 0 && g < kT4TrTiles) tr[T4TR(g, x)] = t4_clk();
+        // S(k) landed => G2(k - NSB) and everything before it completed: the K/V ring slot of
+        // tile g - kRelD (whose last reader is G2(2(g - kRelD) + 1) = G2(k - NSB)) is free.
+        if (x == kRelX && row == 0 && g >= kRelD) ptx::mbar_arrive(&kv_empty[(g - kRelD) % S]);
+        if (p.dbg & 1) {
+          ptx::tc_fence_before();
+          ptx::mbar_arrive(&p_full[b]);
+          continue;
+        }
+        const int valid = n_lim - j * kT4BN;
+        const bool full = valid >= kT4BN;
+        float mx;
+        if (full) {
+          mx = sc >= 0.f ? t4_tile_extreme<false>(tS) : t4_tile_extreme<true>(tS);
+        } else {
+          mx = sc >= 0.f ? t4_tile_extreme_masked<false>(tS, valid) : t4_tile_extreme_masked<true>(tS, valid);
+        }
+        const float m_tile = mx * sc;
+        if (tr && row == 0 && g < kT4TrTiles) tr[T4TR(g, 2 + x)] = t4_clk_after(__float_as_uint(mx));
+        if (j == 0) {
+          m_run = m_tile;
+        } else if (__any_sync(0xffffffffu, m_tile > m_run + kT4Tau)) {
+          // warp-uniform (tcgen05.ld/st are warp-collective).  O_x must hold G2_x(j-1): implied
+          // by s_full for NSB = 2 (G1(k) follows G2(k-2)); an explicit wait for NSB = 3.
+          // NSB = 3: G1(k + 1) is issued right after G2(k + 1 - 3) = G2_x(j - 1), so its S
+          // buffer's phase certifies O_x (the issuer adds a bare commit past the last tile).
+          if constexpr (NSB == 3) ptx::mbar_wait(&s_full[(k + 1) % NSB], ((k + 1) / NSB) & 1);
+          ptx::tc_fence_after();
+          const float m_new = fmaxf(m_run, m_tile);
+          const float alpha = ptx::ex2(m_run - m_new);
+          l2.x *= alpha;
+          l2.y *= alpha;
+          m_run = m_new;
+          for (int c0 = 0; c0 < p.TL; c0 += 16) {
+            uint32_t r[16];
+            ptx::tmem_ld16(tO + c0, r);
+            ptx::tmem_wait_ld();
+#pragma unroll
+            for (int q = 0; q < 16; ++q) r[q] = __float_as_uint(__uint_as_float(r[q]) * alpha);
+            ptx::tmem_st16(tO + c0, r);
+          }
+        }
+        if (full)
+          t4_exp_tile<BF16, EMU, false>(tS, sc, m_run, valid, l2);
+        else
+          t4_exp_tile<BF16, 0, true>(tS, sc, m_run, valid, l2);
+        ptx::tmem_wait_st();
+        if (tr && row == 0 && g < kT4TrTiles) tr[T4TR(g, 4 + x)] = t4_clk();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&p_full[b]);
+      }
+      // The look-ahead G1s let a softmax run more than a unit ahead of the epilogue (units of
+      // one tile), and l_full's parity protocol allows only one phase in flight: publishing l
+      // of unit ai waits until the epilogue has read unit ai - 1's.
+      if (ai >= 1) ptx::mbar_wait(&l_free[x], (ai - 1) & 1);
+      l_sm[x][ai & 1][row] = l2.x + l2.y;
+      ptx::mbar_arrive(&l_full[x]);
+      ++ai;
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (tr && threadIdx.x == 0) tr[3] = ptx::globaltimer();
+  if (warp == 12) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, 512);
+  }
+}
+
+}  // namespace mbci

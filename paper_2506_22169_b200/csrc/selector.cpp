@@ -113,6 +113,23 @@ bool tc3_layout(int32_t k_steps, int32_t TL, int32_t stages, int32_t b_layout, T
   return false;
 }
 
+bool tc4_layout(int32_t k_steps, int32_t TL, int32_t stages, int32_t b_layout, Tc4Layout* out,
+                int32_t smem_max) {
+  if (TL > 128 || k_steps < 1) return false;   // TMEM: NSB S buffers + O_0, O_1
+  if (TL <= 64 && stages < 3) return false;      // NSB = 3 releases K/V slot g at tile g + 2
+  int32_t a, b, d;
+  tc_smem_bytes(k_steps, 128, TL, stages, b_layout, &a, &b, &d);
+  for (int32_t q_bufs = 2; q_bufs >= 1; --q_bufs) {
+    const int32_t bars = 8 * (18 + 3 * stages);
+    const int32_t total = q_bufs * 2 * a + stages * (b + d) + bars + 1024;
+    if (total + 3072 <= smem_max) {   // 2 KB of l + slack stay for static shared memory
+      if (out) *out = Tc4Layout{a, b, d, q_bufs, total};
+      return true;
+    }
+  }
+  return false;
+}
+
 int32_t tmem_alloc_cols(int32_t BN, int32_t TL) {
   const int32_t need = 2 * BN + TL;
   int32_t c = 32;
@@ -140,7 +157,7 @@ static void score_b200(const mbci_chain_desc_t& d, const mbci_hw_t& hw, mbci_pla
   const double rows = static_cast<double>(lm * p.BM), keys = static_cast<double>(nt * p.BN);
   double t_tc, t_sfu = 0.0, t_issue;
   const double elems = b * static_cast<double>(lh) * rows * keys;  // C elements computed
-  if (p.kernel == 0) {
+  if (p.kernel != 1) {   // every tcgen05 family
     t_tc = b * lh * 2.0 * rows * keys * (p.TK + p.TL) / hw.P;
     if (d.op == MBCI_OP_SOFTMAX) t_sfu = elems / (hw.n_sm * hw.sfu_per_clk_sm * hw.clock_hz);
     const double instr = (d.op == MBCI_OP_SOFTMAX) ? 5.0 : 1.5;  // thread-instructions/element
@@ -149,6 +166,15 @@ static void score_b200(const mbci_chain_desc_t& d, const mbci_hw_t& hw, mbci_pla
     // CUDA cores: 2 FMAs per (m,n,k) and (m,n,l), 128 FMA lanes per SM
     t_tc = b * 2.0 * d.M * d.N * (d.K + d.L) / (hw.n_sm * 256.0 * hw.clock_hz);
     t_issue = t_tc;
+  }
+  if (p.kernel == 4) {
+    // persistent pair units dealt round-robin: ceil(units / n_sm) rounds, no stream-K.  The
+    // FMA-pipe polynomial takes 3/8 of the exponentials off the MUFU (chain_tc4.cuh).
+    const double units = static_cast<double>(p.n_block);
+    const double rounds = std::ceil(units / hw.n_sm);
+    const double q4 = units > 0 ? rounds * hw.n_sm / units : 1.0;
+    p.t_b200 = std::max(std::max(t_hbm, t_tc), std::max(t_sfu * 0.625, t_issue * 0.8)) * q4 + 1.0e-6;
+    return;
   }
   if (p.kernel == 2 || p.kernel == 3) {
     // persistent stream-K: work splits evenly over 2 x n_sm slots; one prologue, no waves
@@ -188,6 +214,30 @@ int enumerate_plans(const mbci_chain_desc_t& d, const mbci_hw_t& hw,
         for (int32_t TL = 16; TL <= lpad; TL += 16) {
           if (apply_rule3 && d.L > 0 && rule3_reject(d.L, TL)) continue;
           if (2 * BN + TL > hw.tmem_cols) continue;  // TMEM budget
+          for (int32_t st = 2; st <= 8 && BN == 128 && TL == lpad && d.op == MBCI_OP_SOFTMAX && k_steps >= 1 &&
+                               d.N >= 1; ++st) {
+            Tc4Layout lay4;
+            if (tc4_layout(k_steps, TL, st, d.b_layout, &lay4, hw.smem_max)) {
+              mbci_plan_t p{};
+              p.kernel = 4;
+              p.BM = 256;
+              p.BN = 128;
+              p.TK = 16 * k_steps;
+              p.TL = TL;
+              p.stages = st;
+              p.smem_bytes = lay4.smem_total;
+              p.tmem_cols = 512;
+              double t[5];
+              model_terms(d.batch, d.M, d.N, d.K, d.L, p.BM, p.BN, p.TK, p.TL, s, hw, t);
+              p.t_mem = t[0];
+              p.t_comp = t[1];
+              p.alpha = t[2];
+              p.t_estm = t[3];
+              p.n_block = static_cast<int64_t>(t[4]);
+              score_b200(d, hw, p);
+              out.push_back(p);
+            }
+          }
           for (int32_t st = 2; st <= 8 && BN == 128; ++st) {
             Tc3Layout lay3;
             if (tc3_layout(k_steps, TL, st, d.b_layout, &lay3, hw.smem_max)) {

@@ -28,6 +28,13 @@ struct Tc3Layout {
 };
 bool tc3_layout(int32_t k_steps, int32_t TL, int32_t stages, int32_t b_layout, Tc3Layout* out,
                 int32_t smem_max = 232448);
+// SMEM carve-up of the persistent ping-pong attention kernel (chain_tc4.cuh): Q pair buffers,
+// a K/V ring, barriers (l and the TMEM slot live in static shared memory).
+struct Tc4Layout {
+  int32_t q_bytes, b_stage, d_stage, q_bufs, smem_total;
+};
+bool tc4_layout(int32_t k_steps, int32_t TL, int32_t stages, int32_t b_layout, Tc4Layout* out,
+                int32_t smem_max = 232448);
 // rule3 = false skips Rule 3 entirely: an explicitly forced plan only has to be
 // legal (SMEM / TMEM / TMA), not preferred.
 int enumerate_plans(const mbci_chain_desc_t& d, const mbci_hw_t& hw,

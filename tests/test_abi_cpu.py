@@ -112,10 +112,12 @@ def test_enumerated_plans_are_legal_and_scored(m, shape, b_layout):
     if any(x % 8 for x in (K, b_inner, L)):        # TMA needs 16-byte row strides
         assert [p.kernel for p in plans] == [1]
         return
-    assert {p.kernel for p in plans} <= {0, 2, 3}
+    assert {p.kernel for p in plans} <= {0, 2, 3, 4}
     for p in plans:
-        assert p.kernel in (0, 2, 3) and p.BN in (64, 128)
-        assert p.BM == (256 if p.kernel == 3 else 128)   # kernel 3: two 128-row Q tiles per CTA
+        assert p.kernel in (0, 2, 3, 4) and p.BN in (64, 128)
+        assert p.BM == (256 if p.kernel in (3, 4) else 128)   # kernels 3, 4: two 128-row Q tiles per CTA
+        if p.kernel == 4:    # softmax only, whole L in the CTA
+            assert p.TL == lpad and p.BN == 128
         assert p.TL % 16 == 0 and 16 <= p.TL <= lpad
         assert p.TK == max(16, math.ceil(K / 16) * 16)
         assert p.smem_bytes <= hw.smem_max
@@ -126,6 +128,8 @@ def test_enumerated_plans_are_legal_and_scored(m, shape, b_layout):
         else:                # two Q tiles: S_0, S_1 (128 each) + O_0, O_1
             assert p.tmem_cols == 512 and p.BN == 128 and 256 + 2 * p.TL <= 512
         assert 2 <= p.stages <= (4 if p.kernel == 0 else 8)
+        if p.kernel == 4:
+            assert p.smem_bytes + 3072 <= hw.smem_max
         if rule3_ok:
             assert not model.rule3_reject(N, p.BN)
         ref = model.chain_estimate(b, M, N, K, L, p.BM, p.BN, p.TK, p.TL, 2, hw.W, hw.P, hw.n_sm)
@@ -143,7 +147,7 @@ def test_bert_base_prefers_full_L_tile(m):
     d = m.make_desc(96, 512, 512, 64, 64, "f16", "softmax")
     p = m.mbci_plan_t()
     assert m.mbci_plan_select(ctypes.byref(d), None, ctypes.byref(p)) == m.MBCI_OK
-    assert p.TL == 64 and p.kernel == 0
+    assert p.TL == 64 and p.kernel in (0, 4)
 
 
 def test_fp32_and_misaligned_go_to_cuda_cores(m):

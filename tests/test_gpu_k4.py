@@ -1,0 +1,172 @@
+"""Parity of kernel family 4 (chain_tc4.cuh: persistent ping-pong attention kernel) with the fp64
+oracle, forced through mbci_chain_create_with_plan so every case runs that kernel.
+
+Covers: both B layouts and dtypes, head dims 16..128 (d = 128 single-buffers Q), ragged M
+(a pair unit whose second 128-row tile is entirely past M), ragged N and K/L not multiples of
+16, key padding (0, 1, partial-tile and full lengths, mixed within one launch so CTAs see
+units with different tile counts), the lazy-rescale path, negative / zero scale, rows summing
+to one, more units than CTAs (Q buffers, o_free and the K/V ring cycle many times), both
+exponential paths (MUFU only, and 3/8 of the pairs on the FMA-pipe polynomial), run-to-run
+bitwise determinism, and strided operands.
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import mbci_inputs as gen
+import oracle
+from gpu_helpers import e_f64, run_chain, to_dev
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"f16": 2e-2, "bf16": 2e-2}
+BUDGET = {"f16": 4e-3, "bf16": 1.5e-2}
+
+
+@pytest.fixture(scope="module")
+def mbci():
+    assert torch.cuda.is_available(), "gpu tests need a GPU"
+    from paper_2506_22169_b200 import mbci as m
+    return m
+
+
+@pytest.fixture(params=["0", "3"], ids=["mufu", "poly3of8"])
+def emu(request, monkeypatch):
+    monkeypatch.setenv("MBCI_T4_EMU", request.param)
+    return request.param
+
+
+def k4_plan(mbci, L, stages=None):
+    if stages is None:   # three S buffers (TL <= 64) need a 3-deep K/V ring; d = 128 fits only 2
+        stages = 3 if L <= 64 else 2
+    p = mbci.mbci_plan_t()
+    p.kernel, p.BN, p.TL, p.stages = 4, 128, max(16, (L + 15) // 16 * 16), stages
+    return p
+
+
+def check4(mbci, inp, scale, valid_len=None, stages=None, rows=None):
+    E, ch = run_chain(mbci, inp, "softmax", scale, valid_len, plan=k4_plan(mbci, inp.L, stages))
+    assert ch.plan().kernel == 4, ch.describe()
+    got = e_f64(E, inp.dtype)
+    if rows is not None:
+        ref = oracle.chain(inp, "softmax", scale, valid_len=valid_len, rows=rows)
+        got = got[rows[:, 0], rows[:, 1]]
+    else:
+        ref = oracle.chain(inp, "softmax", scale, valid_len=valid_len)
+    assert np.all(np.isfinite(got)), "non-finite output"
+    err = oracle.row_max_error(got, ref)
+    assert err <= BUDGET[inp.dtype], (err, ch.describe())
+    return E, ch
+
+
+@pytest.mark.parametrize("dtype,b_layout", [("f16", 1), ("bf16", 1), ("f16", 0), ("bf16", 0)])
+def test_k4_bert_base_slice(mbci, emu, dtype, b_layout):
+    inp = gen.make_chain_inputs(1, dtype, 8, 512, 512, 64, 64, b_layout)
+    check4(mbci, inp, 0.125)
+
+
+@pytest.mark.parametrize("K,L", [(16, 16), (32, 64), (64, 128), (128, 128), (128, 32), (80, 80)])
+def test_k4_head_dims(mbci, emu, K, L):
+    inp = gen.make_chain_inputs(K + 3 * L, "bf16", 3, 256, 512, K, L, 1)
+    check4(mbci, inp, 1.0 / math.sqrt(K))
+
+
+@pytest.mark.parametrize("M,N,K,L", [(300, 333, 48, 40), (129, 1000, 72, 56), (1, 1, 16, 16), (384, 130, 8, 8),
+                                     (640, 257, 64, 64)])
+def test_k4_ragged(mbci, emu, M, N, K, L):
+    inp = gen.make_chain_inputs(M + N, "f16", 2, M, N, K, L, 1)
+    check4(mbci, inp, 1.0 / math.sqrt(K))
+
+
+def test_k4_key_padding_mixed(mbci, emu):
+    b = 9
+    inp = gen.make_chain_inputs(5, "f16", b, 256, 512, 64, 64, 1, sigmas=(3.0, 3.0, 1.0))
+    vl = np.array([512, 1, 0, 130, 128, 257, 0, 511, 2], dtype=np.int32)
+    E, _ = check4(mbci, inp, 0.125, valid_len=vl)
+    got = e_f64(E, "f16")
+    D = gen.bits_to_f64_numpy(inp.D, "f16")
+    assert np.array_equal(got[1], np.broadcast_to(D[1, 0], got[1].shape))   # one key: E = D[0,:]
+    assert np.all(got[2] == 0.0) and np.all(got[6] == 0.0)                  # no key: E = 0
+
+
+def test_k4_rescale_path_rising_scores(mbci, emu):
+    base = gen.make_chain_inputs(9, "bf16", 2, 256, 1024, 64, 64, 1)
+    A = gen.bits_to_f64_numpy(base.A, "bf16")
+    B = gen.bits_to_f64_numpy(base.B, "bf16")
+    A[:, :, -1] = 1.0
+
+    def bits(x):
+        return gen._f64_to_storage(x.ravel(), "bf16").reshape(x.shape)
+
+    for gamma in (0.03125, 0.25):
+        B[:, :, -1] = gamma * np.arange(1024)[None, :]
+        inp = gen.ChainInputs(bits(A), bits(B), base.D, None, "bf16", 2, 256, 1024, 64, 64, 1)
+        check4(mbci, inp, 1.0)
+
+
+def test_k4_negative_and_zero_scale(mbci, emu):
+    inp = gen.make_chain_inputs(12, "bf16", 2, 256, 384, 64, 64, 1)
+    check4(mbci, inp, -0.125)
+    check4(mbci, inp, 0.0)
+
+
+def test_k4_rows_sum_to_one(mbci, emu):
+    inp = gen.make_chain_inputs(11, "f16", 4, 256, 384, 64, 64, 1, sigmas=(2.0, 2.0, 1.0))
+    inp.D = np.ascontiguousarray(np.full(inp.D.shape, 0x3C00, dtype=np.uint16))
+    E, _ = run_chain(mbci, inp, "softmax", 0.125, plan=k4_plan(mbci, 64))
+    assert np.max(np.abs(e_f64(E, "f16") - 1.0)) <= 2 * 2.0 ** -11 + 1e-6
+
+
+@pytest.mark.parametrize("stages", [3, 4, 5])   # 5 stages leave room for one Q-pair buffer only
+def test_k4_many_units_per_cta(mbci, emu, stages):
+    """600 pair units on <= 148 CTAs: every Q buffer, the K/V ring and o_free cycle many times;
+    key lengths vary per β so CTAs interleave units of 0..3 tiles."""
+    b, M, N = 600, 256, 384
+    inp = gen.make_chain_inputs(21, "f16", b, M, N, 64, 64, 1, valid_len_range=(0, N))
+    rows = np.stack([np.arange(b), (np.arange(b) * 37) % M], axis=1).astype(np.int64)
+    check4(mbci, inp, 0.125, valid_len=inp.valid_len, stages=stages, rows=rows)
+
+
+def test_k4_wide_head_two_stages(mbci, emu):
+    """TL > 64 keeps two S buffers (NSB = 2), whose K/V release needs only two ring stages."""
+    inp = gen.make_chain_inputs(23, "bf16", 300, 256, 384, 128, 128, 1)
+    rows = np.stack([np.arange(300), (np.arange(300) * 53) % 256], axis=1).astype(np.int64)
+    check4(mbci, inp, 1.0 / math.sqrt(128), stages=2, rows=rows)
+
+
+def test_k4_deterministic(mbci, emu):
+    inp = gen.make_chain_inputs(17, "f16", 16, 512, 512, 64, 64, 1)
+    E1, _ = run_chain(mbci, inp, "softmax", 0.125, plan=k4_plan(mbci, 64))
+    E2, _ = run_chain(mbci, inp, "softmax", 0.125, plan=k4_plan(mbci, 64))
+    assert torch.equal(E1.view(torch.int16), E2.view(torch.int16))
+
+
+def test_k4_strided_operands(mbci):
+    b, M, N, K, L = 3, 200, 320, 64, 48
+    inp = gen.make_chain_inputs(16, "f16", b, M, N, K, L, 1)
+
+    def pad(x, ld, bs):
+        out = np.zeros(b * bs, dtype=np.uint16)
+        rows, cols = x.shape[1], x.shape[2]
+        v = out.reshape(b, bs)
+        for i in range(b):
+            v[i, :rows * ld].reshape(rows, ld)[:, :cols] = x[i]
+        return out
+
+    ldA, bsA, ldB, bsB, ldD, bsD, ldE, bsE = 72, 72 * 200 + 64, 80, 80 * 320, 56, 56 * 320 + 8, 64, 64 * 200 + 16
+    A, B, D = (to_dev(pad(inp.A, ldA, bsA), "f16"), to_dev(pad(inp.B, ldB, bsB), "f16"),
+               to_dev(pad(inp.D, ldD, bsD), "f16"))
+    E = torch.full((b * bsE,), float("nan"), dtype=torch.float16, device="cuda")
+    ch = mbci.Chain(b, M, N, K, L, "f16", "softmax", 0.125, b_layout=1, plan=k4_plan(mbci, L),
+                    strides=dict(ld_a=ldA, bs_a=bsA, ld_b=ldB, bs_b=bsB, ld_d=ldD, bs_d=bsD, ld_e=ldE, bs_e=bsE))
+    assert ch.plan().kernel == 4
+    ch.run(A, B, D, E)
+    torch.cuda.synchronize()
+    Ef = E.cpu().float().numpy().astype(np.float64).reshape(b, bsE)
+    got = np.stack([Ef[i, :M * ldE].reshape(M, ldE)[:, :L] for i in range(b)])
+    assert np.all(np.isnan(Ef[0, M * ldE:]))
+    assert np.all(np.isnan(Ef[0, :ldE * M].reshape(M, ldE)[:, L:]))
+    assert oracle.row_max_error(got, oracle.chain(inp, "softmax", 0.125)) <= BUDGET["f16"]

@@ -1,0 +1,122 @@
+// tcgen05.mma throughput on ALL SMs with non-zero data, in the shapes kernel 4 issues:
+//   G1 = 4 x SS (M=128, N=128, K=16) and G2 = 8 x TS (M=128, N=64, K=16, B MN-major), each group
+//   followed by tcgen05.commit; variants wait for every commit (latency) or only at the end.
+#include <cstdio>
+#include <cstdint>
+#include <cuda.h>
+#include "../paper_2506_22169_b200/csrc/ptx.cuh"
+using namespace mbci;
+__global__ void __launch_bounds__(384, 1) k(int mode, int rounds, int bg, uint64_t* out) {
+  __shared__ volatile int done_flag;
+  extern __shared__ uint8_t raw[];
+  uint8_t* sm = (uint8_t*)(((uintptr_t)raw + 1023) & ~(uintptr_t)1023);
+  __shared__ uint64_t bar, bar2, bar3;
+  __shared__ uint32_t tslot;
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) { ptx::mbar_init(&bar, 1); ptx::mbar_init(&bar2, 1); ptx::mbar_arrive(&bar2); ptx::mbar_init(&bar3, 1); ptx::fence_mbar_init(); done_flag = 0; }
+  uint32_t seed = 0x9e3779b9u * (threadIdx.x + 1) + blockIdx.x;
+  for (int i = threadIdx.x; i < 98304 / 4; i += blockDim.x) {
+    seed = seed * 1664525u + 1013904223u;
+    const uint32_t h = 0x3800u | ((seed >> 16) & 0x3ffu), l = 0x3800u | (seed & 0x3ffu);   // fp16 in [0.5, 1)
+    ((uint32_t*)sm)[i] = (h << 16) | l;
+  }
+  if (warp == 1) ptx::tmem_alloc(&tslot, 512);
+  asm volatile("fence.proxy.async.shared::cta;");
+  ptx::tc_fence_before(); __syncthreads(); ptx::tc_fence_after();
+  const uint32_t tmem = tslot;
+  if (warp < 4) {  // P region: fill TMEM columns [0, 64) of every lane with fp16 pairs
+    uint32_t r[32];
+    for (int q = 0; q < 32; ++q) r[q] = 0x38003800u + q;
+    ptx::tmem_st32(tmem + ((uint32_t)(warp * 32) << 16), r);
+    ptx::tmem_st32(tmem + ((uint32_t)(warp * 32) << 16) + 32, r);
+    ptx::tmem_wait_st();
+  }
+  ptx::tc_fence_before(); __syncthreads(); ptx::tc_fence_after();
+  if (warp == 1 && ptx::elect_one()) {
+    const uint32_t id1 = ptx::idesc_f16(0, 0, 0, 128, 128);
+    const uint32_t id2 = ptx::idesc_f16(0, 0, 1, 128, 64);
+    const uint32_t q0 = ptx::smem_u32(sm), k0 = ptx::smem_u32(sm + 16384), v0 = ptx::smem_u32(sm + 32768);
+    const uint64_t dA = ptx::sdesc_sw128(0, 16, 1024), dD = ptx::sdesc_sw128(0, 128 * 128, 1024);
+    uint32_t ph = 0;
+    const uint64_t c0 = clock64(), t0 = ptx::globaltimer();
+    for (int r = 0; r < rounds; ++r) {
+      if (mode & 16) ptx::tc_fence_after();
+      if (mode & 32) { ptx::mbar_spin(&bar2, 0); }
+      if (mode & 1) {   // G1
+        for (int ks = 0; ks < 4; ++ks)
+          ptx::mma_ss(tmem + 128, dA + ((q0 + ks * 32) >> 4), dA + ((k0 + ks * 32) >> 4), id1, ks > 0);
+        if (mode & 4) { ptx::mma_commit(&bar); ptx::mbar_spin(&bar, ph); ph ^= 1; }
+      }
+      if (mode & 16) ptx::tc_fence_after();
+      if (mode & 32) { ptx::mbar_spin(&bar2, 0); }
+      if (mode & 2) {   // G2
+        for (int ks = 0; ks < 8; ++ks)
+          ptx::mma_ts(tmem + 384, tmem + ks * 8, dD + ((v0 + ks * 2048) >> 4), id2, 1);
+        if (mode & 4) { ptx::mma_commit(&bar); ptx::mbar_spin(&bar, ph); ph ^= 1; }
+      }
+      if (mode & 8) ptx::mma_commit(&bar), ph ^= 1;   // an extra un-awaited commit per round
+    }
+    ptx::mma_commit(&bar);
+    ptx::mbar_spin(&bar, ph);
+    const uint64_t c1 = clock64(), t1 = ptx::globaltimer();
+    out[2 * blockIdx.x] = c1 - c0;
+    out[2 * blockIdx.x + 1] = t1 - t0;
+    done_flag = 1;
+  } else if (warp >= 4 && bg) {
+    // background: warps 4-11 (two per SMSP) like the softmax warpgroups: bg&1 MUFU+FFMA2 work,
+    // bg&2 tcgen05.ld of a 128-column S region (lanes of this warp's quadrant)
+    const uint32_t tS = tmem + 128 + ((uint32_t)((warp & 3) * 32) << 16);
+    float2 acc = make_float2(threadIdx.x * 1e-3f, 1.f);
+    float y = 0.f;
+    while (!done_flag) {
+      if (bg & 2) {
+        uint32_t r[32];
+        ptx::tmem_ld32(tS, r);
+        ptx::tmem_ld32(tS + 32, r);
+        ptx::tmem_wait_ld();
+        y += __uint_as_float(r[5]);
+      }
+      if (bg & 4) {   // poll an mbarrier phase that never completes (like warps blocked in mbar_wait)
+        for (int i = 0; i < 64; ++i) y += ptx::mbar_try_wait(ptx::smem_u32(&bar3), 0) ? 1.f : 0.f;
+      }
+      if (bg & 8) {   // same with test_wait (non-suspending)
+        for (int i = 0; i < 64; ++i) y += ptx::mbar_test(&bar3, 0) ? 1.f : 0.f;
+      }
+      if (bg & 1) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          acc = __ffma2_rn(acc, make_float2(0.999f, 0.999f), make_float2(1e-4f, 2e-4f));
+          y += ptx::ex2(acc.x) + ptx::ex2(acc.y);
+        }
+      }
+    }
+    if (y == 1234.5f) out[0] = 0;
+  }
+  ptx::tc_fence_before(); __syncthreads();
+  if (warp == 1) { ptx::tc_fence_after(); ptx::tmem_dealloc(tmem, 512); }
+}
+int main() {
+  uint64_t* d; cudaMalloc(&d, 148 * 16);
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100000);
+  auto name = [](int m) {
+    static char b[128];
+    snprintf(b, sizeof b, "%s%s%s%s%s", (m & 1) ? "G1 " : "", (m & 2) ? "G2 " : "", (m & 4) ? "+commit/wait " : "",
+             (m & 16) ? "+fence::after " : "", (m & 32) ? "+test_wait(done bar) " : "");
+    return b;
+  };
+  const char* bgn[] = {"idle", "MUFU+FMA", "TMEM ld", "MUFU+FMA+TMEM ld", "try_wait poll", "", "", "", "test_wait poll"};
+  for (int bg : {0, 4, 8})
+    for (int mode : {3, 7, 3 | 32}) {
+      const int grid = 148, rounds = 200;
+      k<<<grid, 384, 100000>>>(mode, rounds, bg, d);
+      k<<<grid, 384, 100000>>>(mode, rounds, bg, d);
+      cudaError_t e = cudaDeviceSynchronize();
+      uint64_t h[296]; cudaMemcpy(h, d, grid * 16, cudaMemcpyDeviceToHost);
+      double cyc = 0, ns = 0;
+      for (int i = 0; i < grid; ++i) { cyc += h[2 * i]; ns += h[2 * i + 1]; }
+      cyc /= grid; ns /= grid;
+      const int mmas = ((mode & 1) ? 4 : 0) + ((mode & 2) ? 8 : 0);
+      printf("bg %-18s %-26s %7.1f cyc/round  %6.1f cyc/MMA  %5.0f MHz effective  (%s)\n", bgn[bg], name(mode),
+             cyc / rounds, cyc / rounds / mmas, cyc / ns * 1e3, cudaGetErrorString(e));
+    }
+}
