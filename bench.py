@@ -319,7 +319,7 @@ def run_cuda(args, rank, world, local_rank):
     traffic = _traffic(name, world)
     roofline = {"bound": "hbm", "achieved": gbs / world, "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": frac, "traffic": traffic, "peak_src": pk["src"],
-                "kernel": "k_chain_tc" if plan.kernel == 0 else "k_chain_simt",
+                "kernel": {0: "k_chain_tc", 1: "k_chain_simt", 2: "k_chain_tc2", 3: "k_chain_tc3", 4: "k_chain_tc4"}.get(plan.kernel, "?"),
                 "per_launch_bytes": step_bytes, "per_launch_us": ms_per_step * 1e3,
                 "tensor_tflops": tflops / world, "tensor_frac": tflops / world / pk["bf16_tflops"],
                 "ex2_per_s": (exps * nb / b) / (ms_per_step * 1e-3) if exps else 0.0}

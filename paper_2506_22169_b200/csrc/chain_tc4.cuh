@@ -27,8 +27,8 @@
 //   exact in real arithmetic (R4).
 //
 // Warps: 0-3 softmax slot 0 | 4-7 softmax slot 1 | 8-11 epilogue | 12 tcgen05 issuer + TMEM
-//        allocator | 13 TMA producer | 14-15 idle.  Every role fits in the 128 registers of a
-//        512-thread CTA (the softmax streams S through registers 32-64 columns at a time).
+//        allocator | 13 TMA producer | 14-15 idle.  setmaxnreg moves registers to the softmax
+//        warpgroups (184 each: a whole 128-column S row in registers) from the others (80 / 64).
 #pragma once
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -57,6 +57,13 @@ struct Tc4Params {
   uint32_t q_bytes;        // one 128-row Q tile
   uint32_t b_stage_bytes, d_stage_bytes, kp_rows;
   uint32_t idesc1, idesc2;
+  // Work items (one per CTA round): items [0, tail) are whole pair units; the last r = units -
+  // tail units are cut along the key axis into `pieces` items of `piece_tiles` 128-key tiles,
+  // so the final round fills the SMs (wave quantisation).  Each piece stores its partial
+  // (O, m, l) to `ws`; the last piece to finish (atomic count in `cnt`) merges them.
+  int32_t items, tail, pieces, piece_tiles, nt_max;
+  float* ws;               // [r * pieces][256][TL] O, then m [r * pieces][256], l [r * pieces][256]
+  int32_t* cnt;            // [r][2], zero between launches
   uint64_t* trace;         // [gridDim.x][kT4TraceSlots] (MBCI_TRACE builds only)
   int32_t dbg;             // diagnostics only (MBCI_T4_DEBUG): 1 = softmax skips its TMEM/math work,
                            // 2 = issuer skips the G2 MMAs, 4 = issuer skips the G1 MMAs
@@ -65,6 +72,7 @@ struct Tc4Params {
 constexpr int kT4Threads = 512;
 constexpr int kT4BN = 128;
 constexpr float kT4Tau = 8.0f;
+constexpr int kT4MaxPieces = 4;   // key-axis pieces per tail unit (api.cu caps the split)
 constexpr int kT4TraceSlots = 512;
 // trace layout per CTA (MBCI_TRACE builds): [0] start (globaltimer ns) [1] setup [2] smid [3] end,
 // [4] clock64 at start; per flat tile g < 40 and slot x, SM clock64 at 8 + 12*g + {0+x: S ready,
@@ -90,6 +98,27 @@ __device__ __forceinline__ int t4_nlim(const Tc4Params& p, int beta) {
   return n;
 }
 
+// Work item i -> pair unit u, its key-tile range [t0, t1) and piece index (-1: whole unit).
+struct T4Item {
+  int u, t0, t1, piece;
+  __device__ __forceinline__ void decode(const Tc4Params& p, int i) {
+    if (i < p.tail) {
+      u = i; t0 = 0; t1 = p.nt_max; piece = -1;
+    } else {
+      const int q = i - p.tail;
+      u = p.tail + q / p.pieces;
+      piece = q - (u - p.tail) * p.pieces;
+      t0 = piece * p.piece_tiles;
+      t1 = min(t0 + p.piece_tiles, p.nt_max);
+    }
+  }
+  // valid tiles of this item given the unit's key limit
+  __device__ __forceinline__ int tiles(int n_lim) const {
+    const int ntv = (n_lim + kT4BN - 1) / kT4BN;
+    return max(0, min(t1, ntv) - t0);
+  }
+};
+
 // 2^x for a pair, on the FMA/ALU pipes.  x <= 2^22; results below 2^-127 flush towards 0.
 //   x = n + f, n = floor(x) (round-down add of 1.5·2^23), f in [0, 1);
 //   2^f ~= ((c3 f + c2) f + c1) f + c0 (minimax, relative error 8.8e-5); 2^n by exponent add.
@@ -110,81 +139,52 @@ __device__ __forceinline__ float2 t4_exp2_poly(float2 x) {
   return r;
 }
 
-// Row extreme of a 128-column S tile in TMEM (max, or min when the scale is negative), read in
-// two 64-column halves so that no more than 64 scores are live in registers.
+// Row extreme of a 128-column S row held in registers (max, or min when the scale is negative):
+// eight independent FMNMX3 chains.  MASKED: only the first `valid` (< 128) columns count (keys
+// n >= n_lim are −inf before the softmax).
 template <bool MIN>
 __device__ __forceinline__ float t4_red(float a, float b, float c) {
   return MIN ? ptx::min3(a, b, c) : ptx::max3(a, b, c);
 }
-template <bool MIN>
-__device__ __forceinline__ float t4_tile_extreme(uint32_t tS) {
-  float a0, a1, a2, a3;
+template <bool MIN, bool MASKED>
+__device__ __forceinline__ float t4_row_extreme(const uint32_t (&sr)[kT4BN], int valid) {
+  if constexpr (MASKED) {
+    float mx = MIN ? INFINITY : -INFINITY;
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    uint32_t r[64];
-    ptx::tmem_ld32(tS + h * 64, r);
-    ptx::tmem_ld32(tS + h * 64 + 32, r + 32);
-    ptx::tmem_wait_ld();
-    int c0 = 0;
-    if (h == 0) {
-      a0 = __uint_as_float(r[0]);
-      a1 = __uint_as_float(r[1]);
-      a2 = __uint_as_float(r[2]);
-      a3 = __uint_as_float(r[3]);
-      c0 = 4;
+    for (int c = 0; c < kT4BN; ++c) {
+      const float v = __uint_as_float(sr[c]);
+      if (c < valid) mx = MIN ? fminf(mx, v) : fmaxf(mx, v);
     }
+    return mx;
+  } else {
+    float a[8];
 #pragma unroll
-    for (int c = c0; c < 64; c += 8) {
-      a0 = t4_red<MIN>(a0, __uint_as_float(r[c]), __uint_as_float(r[c + 1]));
-      a1 = t4_red<MIN>(a1, __uint_as_float(r[c + 2]), __uint_as_float(r[c + 3]));
-      if (c + 4 < 64) {
-        a2 = t4_red<MIN>(a2, __uint_as_float(r[c + 4]), __uint_as_float(r[c + 5]));
-        a3 = t4_red<MIN>(a3, __uint_as_float(r[c + 6]), __uint_as_float(r[c + 7]));
-      }
-    }
+    for (int q = 0; q < 8; ++q)
+      a[q] = MIN ? fminf(__uint_as_float(sr[2 * q]), __uint_as_float(sr[2 * q + 1]))
+                 : fmaxf(__uint_as_float(sr[2 * q]), __uint_as_float(sr[2 * q + 1]));
+#pragma unroll
+    for (int c = 16; c < kT4BN; c += 16)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) a[q] = t4_red<MIN>(a[q], __uint_as_float(sr[c + 2 * q]), __uint_as_float(sr[c + 2 * q + 1]));
+    return t4_red<MIN>(t4_red<MIN>(a[0], a[1], a[2]), t4_red<MIN>(a[3], a[4], a[5]), MIN ? fminf(a[6], a[7]) : fmaxf(a[6], a[7]));
   }
-  return t4_red<MIN>(a0, a1, MIN ? fminf(a2, a3) : fmaxf(a2, a3));
-}
-// Same over the first `valid` (< 128) columns only: keys n >= n_lim are masked (−inf).
-template <bool MIN>
-__device__ __forceinline__ float t4_tile_extreme_masked(uint32_t tS, int valid) {
-  float mx = MIN ? INFINITY : -INFINITY;
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    uint32_t r[64];
-    ptx::tmem_ld32(tS + h * 64, r);
-    ptx::tmem_ld32(tS + h * 64 + 32, r + 32);
-    ptx::tmem_wait_ld();
-#pragma unroll
-    for (int c = 0; c < 64; ++c) {
-      const float v = __uint_as_float(r[c]);
-      if (h * 64 + c < valid) mx = MIN ? fminf(mx, v) : fmaxf(mx, v);
-    }
-  }
-  return mx;
 }
 
-// p = 2^(sc·S − m) over the 128 columns of S_x, written back as 16-bit P into columns
-// [0, 64) of S_x (each 32-column S chunk becomes 16 packed columns, which only overwrite
-// S columns already read).  The next chunk's tcgen05.ld is in flight while the current one is
-// exponentiated.  MASKED: columns >= valid give p = 0.
+// p = 2^(sc·S − m) for the 128 scores of the row (registers), accumulated into two packed
+// partial sums, written back as 16-bit P into TMEM columns [0, 64) of the S buffer, 16 columns
+// per tcgen05.st.  MASKED: columns >= valid give p = 0.
 template <bool BF16, int EMU, bool MASKED>
-__device__ __forceinline__ void t4_exp_tile(uint32_t tS, float sc, float m, int valid, float2& l2) {
+__device__ __forceinline__ void t4_exp_row(uint32_t tS, const uint32_t (&sr)[kT4BN], float sc, float m, int valid,
+                                           float2& l2a, float2& l2b) {
   const float2 sc2 = make_float2(sc, sc);
   const float2 nm2 = make_float2(-m, -m);
-  uint32_t ra[32], rb[32];
-  ptx::tmem_ld32(tS, ra);
-  ptx::tmem_wait_ld();
 #pragma unroll
   for (int ch = 0; ch < 4; ++ch) {
-    uint32_t* cur = (ch & 1) ? rb : ra;
-    uint32_t* nxt = (ch & 1) ? ra : rb;
-    if (ch < 3) ptx::tmem_ld32(tS + (ch + 1) * 32, nxt);
     uint32_t pk[16];
 #pragma unroll
     for (int c = 0; c < 16; ++c) {
-      const float2 z = __ffma2_rn(make_float2(__uint_as_float(cur[2 * c]), __uint_as_float(cur[2 * c + 1])), sc2, nm2);
       const int cp = ch * 16 + c;   // pair index in the tile
+      const float2 z = __ffma2_rn(make_float2(__uint_as_float(sr[2 * cp]), __uint_as_float(sr[2 * cp + 1])), sc2, nm2);
       float2 e;
       if (EMU > 0 && ((cp * EMU) & 7) < EMU) {
         e = t4_exp2_poly(z);
@@ -196,11 +196,10 @@ __device__ __forceinline__ void t4_exp_tile(uint32_t tS, float sc, float m, int 
         e.x = (2 * cp < valid) ? e.x : 0.f;
         e.y = (2 * cp + 1 < valid) ? e.y : 0.f;
       }
-      l2 = __fadd2_rn(l2, e);
+      if (c & 1) l2b = __fadd2_rn(l2b, e); else l2a = __fadd2_rn(l2a, e);
       pk[c] = ptx::pack2<BF16>(e.x, e.y);
     }
     ptx::tmem_st16(tS + ch * 16, pk);
-    if (ch < 3) ptx::tmem_wait_ld();
   }
 }
 
@@ -209,18 +208,24 @@ __device__ __forceinline__ void t4_exp_tile(uint32_t tS, float sc, float m, int 
 // qph) and active-unit index ai, and the K/V ring stage (st, parity sph) of the tile.  Per tile
 // the issuer only increments counters; divisions happen once per unit.
 struct T4Cursor {
-  int u, nt, j, ai, qb, qph, st, sph, g;
+  int i, u, t0, nt, j, ai, qb, qph, st, sph, g;
   bool valid;
   __device__ __forceinline__ void skip(const Tc4Params& p, int G) {
-    while (u < p.units) {
-      nt = (t4_nlim(p, u / p.l_mp) + kT4BN - 1) / kT4BN;
-      if (nt > 0) return;
-      u += G;
+    while (i < p.items) {
+      T4Item it;
+      it.decode(p, i);
+      nt = it.tiles(t4_nlim(p, it.u / p.l_mp));
+      if (nt > 0) {
+        u = it.u;
+        t0 = it.t0;
+        return;
+      }
+      i += G;
     }
     valid = false;
   }
   __device__ __forceinline__ void init(const Tc4Params& p, int G) {
-    u = blockIdx.x; j = 0; ai = 0; qb = 0; qph = 0; st = 0; sph = 0; g = 0; valid = true; nt = 0;
+    i = blockIdx.x; j = 0; ai = 0; qb = 0; qph = 0; st = 0; sph = 0; g = 0; valid = true; nt = 0;
     skip(p, G);
   }
   __device__ __forceinline__ void advance(const Tc4Params& p, int G) {
@@ -230,7 +235,7 @@ struct T4Cursor {
       j = 0;
       ++ai;
       if (++qb == p.q_bufs) { qb = 0; qph ^= 1; }
-      u += G;
+      i += G;
       skip(p, G);
     }
   }
@@ -252,7 +257,8 @@ __global__ void __launch_bounds__(kT4Threads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   __shared__ uint32_t tmem_base_slot;
-  __shared__ float l_sm[2][2][128];   // [slot][active-unit parity][row]
+  __shared__ float l_sm[2][2][128];   // [slot][active-item parity][row]: row sum of p
+  __shared__ float m_sm[2][2][128];   // running max (log2 units) the p were taken against
 
   constexpr uint32_t kOCol = NSB * 128;                 // O_0 column; O_1 at kOCol + kOStride
   constexpr uint32_t kOStride = NSB == 3 ? 64 : 128;
@@ -272,11 +278,12 @@ __global__ void __launch_bounds__(kT4Threads, 1)
   uint64_t* o_free = bars + 6;      // [2] epilogue read O_x (128 arrivals)
   uint64_t* l_full = bars + 8;      // [2] softmax x published l (128 arrivals)
   uint64_t* l_free = bars + 10;     // [2] epilogue read l_sm[x][ai & 1] (128 arrivals)
+  __shared__ uint64_t dbg_bar;      // MBCI_T4_DEBUG & 8: per-group MMA latency probe
   uint64_t* s_full = bars + 12;     // [NSB] G1 landed in S buffer b
   uint64_t* p_full = s_full + 3;    // [NSB] softmax wrote P into buffer b (128 arrivals)
-  uint64_t* k_full = p_full + 3;    // [S]
-  uint64_t* v_full = k_full + S;    // [S]
-  uint64_t* kv_empty = v_full + S;  // [S] both G2 of the tile completed (softmax arrival)
+  uint64_t* kv_full = p_full + 3;   // [S] K_g and V_g landed (one barrier: G1 of tile g, which
+                                    // precedes both G2 of the tile, is the only waiter)
+  uint64_t* kv_empty = kv_full + S; // [S] both G2 of the tile completed (softmax arrival)
 
   const int warp = threadIdx.x >> 5;
 #if MBCI_TRACE
@@ -304,9 +311,9 @@ __global__ void __launch_bounds__(kT4Threads, 1)
       ptx::mbar_init(&s_full[b], 1);
       ptx::mbar_init(&p_full[b], 128);
     }
+    ptx::mbar_init(&dbg_bar, 1);
     for (int s = 0; s < S; ++s) {
-      ptx::mbar_init(&k_full[s], 1);
-      ptx::mbar_init(&v_full[s], 1);
+      ptx::mbar_init(&kv_full[s], 1);
       ptx::mbar_init(&kv_empty[s], 1);
     }
     ptx::fence_mbar_init();
@@ -325,14 +332,17 @@ __global__ void __launch_bounds__(kT4Threads, 1)
   const int G = gridDim.x;
 
   if (warp >= 12) {
+    ptx::setmaxnreg_dec<64>();
     if (warp == 13) {
       // ============================================================ TMA producer
       if (ptx::elect_one()) {
         int g = 0, ai = 0;
-        for (int u = blockIdx.x; u < p.units; u += G) {
-          const int beta = u / p.l_mp;
-          const int m0 = (u - beta * p.l_mp) * 256;
-          const int nt = (t4_nlim(p, beta) + kT4BN - 1) / kT4BN;
+        for (int i = blockIdx.x; i < p.items; i += G) {
+          T4Item it;
+          it.decode(p, i);
+          const int beta = it.u / p.l_mp;
+          const int m0 = (it.u - beta * p.l_mp) * 256;
+          const int nt = it.tiles(t4_nlim(p, beta));
           if (nt == 0) continue;
           const int qb = ai % p.q_bufs;
           if (ai >= p.q_bufs) ptx::mbar_wait(&q_empty[qb], ((ai / p.q_bufs) - 1) & 1);
@@ -345,26 +355,25 @@ __global__ void __launch_bounds__(kT4Threads, 1)
               ptx::tma_load_3d(dst + c * 16384, &tmA, &q_full[qb], c * 64, m0 + x * 128, beta);
           }
           ++ai;
-          for (int j = 0; j < nt; ++j, ++g) {
+          for (int j = it.t0; j < it.t0 + nt; ++j, ++g) {
             const int s = g % S;
             if (g >= S) ptx::mbar_wait(&kv_empty[s], ((g / S) - 1) & 1);
             uint8_t* kdst = sKV + s * kv_stage;
             uint8_t* vdst = kdst + p.b_stage_bytes;
             if (tr && g < kT4TrTiles) tr[460 + g] = t4_clk();   // K/V load of tile g issued
-            ptx::mbar_arrive_expect_tx(&k_full[s], p.b_stage_bytes);
+            ptx::mbar_arrive_expect_tx(&kv_full[s], p.b_stage_bytes + p.d_stage_bytes);
             if constexpr (BL == 1) {
 #pragma unroll
               for (int c = 0; c < KCH; ++c)
-                ptx::tma_load_3d(kdst + c * (kT4BN * 128), &tmB, &k_full[s], c * 64, j * kT4BN, beta);
+                ptx::tma_load_3d(kdst + c * (kT4BN * 128), &tmB, &kv_full[s], c * 64, j * kT4BN, beta);
             } else {
 #pragma unroll
               for (int c = 0; c < kT4BN / 64; ++c)
-                ptx::tma_load_3d(kdst + c * (p.kp_rows * 128), &tmB, &k_full[s], j * kT4BN + c * 64, 0, beta);
+                ptx::tma_load_3d(kdst + c * (p.kp_rows * 128), &tmB, &kv_full[s], j * kT4BN + c * 64, 0, beta);
             }
-            ptx::mbar_arrive_expect_tx(&v_full[s], p.d_stage_bytes);
 #pragma unroll
             for (int c = 0; c < DCH; ++c)
-              ptx::tma_load_3d(vdst + c * (kT4BN * 128), &tmD, &v_full[s], c * 64, j * kT4BN, beta);
+              ptx::tma_load_3d(vdst + c * (kT4BN * 128), &tmD, &kv_full[s], c * 64, j * kT4BN, beta);
           }
         }
       }
@@ -383,8 +392,9 @@ __global__ void __launch_bounds__(kT4Threads, 1)
         int b1 = 0, b2 = 0, pph = 0;   // S buffer of the next G1 / G2, p_full parity of b2
         int x1 = 0;                    // slot of the next G1
         bool tail_committed = false;
+        uint32_t dbg_ph = 0;
         // G1: S_b1 = Q_x1 · K_(c1 tile)
-        auto issue_g1 = [&]() {
+        auto issue_g1 = [&](bool kv_ready) {
           if (!c1.valid) {
             // past the CTA's last tile: one bare commit on the next buffer's s_full, so a lazy
             // rescale of the last slot-tile (which waits for "G1(k + 1)") still completes
@@ -395,10 +405,11 @@ __global__ void __launch_bounds__(kT4Threads, 1)
           if (x1 == 0) {
             if (tr && c1.g < kT4TrTiles) tr[T4TR(c1.g, 12)] = t4_clk();
             if (c1.j == 0) ptx::mbar_spin(&q_full[c1.qb], c1.qph);
-            ptx::mbar_spin(&k_full[c1.st], c1.sph);
+            if (!kv_ready) ptx::mbar_spin(&kv_full[c1.st], c1.sph);
             if (tr && c1.g < kT4TrTiles) tr[T4TR(c1.g, 13)] = t4_clk();
             ptx::tc_fence_after();
           }
+            const uint64_t tg1 = t4_clk();
           const uint32_t q_lo = (sQ0 + (c1.qb * 2 + x1) * p.q_bytes) >> 4;
           const uint32_t k_lo = (sKV0 + c1.st * kv_stage) >> 4;
           const uint32_t dS = tmem + b1 * 128;
@@ -412,6 +423,12 @@ __global__ void __launch_bounds__(kT4Threads, 1)
             }
           }
           ptx::mma_commit(&s_full[b1]);
+          if (p.dbg & 8) {   // latency probe: issue -> completion of this G1
+            ptx::mma_commit(&dbg_bar);
+            ptx::mbar_spin(&dbg_bar, dbg_ph);
+            dbg_ph ^= 1;
+            if (tr && c1.g < kT4TrTiles) tr[T4TR(c1.g, 12 + x1)] = t4_clk() - tg1;
+          }
           if (tr && c1.g < kT4TrTiles) tr[T4TR(c1.g, 10 + x1)] = t4_clk();
           if (++b1 == NSB) b1 = 0;
           if (x1 == 1) {
@@ -421,87 +438,196 @@ __global__ void __launch_bounds__(kT4Threads, 1)
           x1 ^= 1;
         };
 #pragma unroll 1
-        for (int i = 0; i < NSB; ++i) issue_g1();
+        for (int i = 0; i < NSB; ++i) issue_g1(false);
         int x2 = 0;
+        bool p_ready = false;
+        // Each mbarrier probe costs the issuer ~100-200 cycles of latency; the probes for the
+        // next step are issued early (their predicates consumed later) so the latency overlaps
+        // the MMAs already queued (~8 deep, tools/mma_issue_bench.cu).
         while (c2.valid) {
           if (tr && c2.g < kT4TrTiles) tr[T4TR(c2.g, 14 + x2)] = t4_clk();
-          ptx::mbar_spin(&p_full[b2], pph);
+          if (!p_ready) ptx::mbar_spin(&p_full[b2], pph);
           if (tr && c2.g < kT4TrTiles) tr[T4TR(c2.g, 6 + x2)] = t4_clk();
           if (c2.j == 0 && c2.ai > 0) ptx::mbar_spin(&o_free[x2], (c2.ai - 1) & 1);
-          if (x2 == 0) ptx::mbar_spin(&v_full[c2.st], c2.sph);
           ptx::tc_fence_after();
+          const bool kv_ready = c1.valid && x1 == 0 && c1.j != 0 ? ptx::mbar_test(&kv_full[c1.st], c1.sph) : false;
           // G2: O_x2 (+)= P_b2 · V_(c2 tile)
           const uint32_t v_lo = (sKV0 + c2.st * kv_stage + p.b_stage_bytes) >> 4;
           const uint32_t tO = tmem + kOCol + x2 * kOStride;
           const uint32_t tP = tmem + b2 * 128;
           const uint32_t acc0 = c2.j > 0 ? 1u : 0u;
+          const uint64_t tg2 = t4_clk();
 #pragma unroll
           for (int ks = 0; ks < kT4BN / 16; ++ks)
             if (!(p.dbg & 2)) ptx::mma_ts(tO, tP + ks * 8, dD + v_lo + ks * 128, idesc2, ks > 0 ? 1u : acc0);
+          if (p.dbg & 8) {   // latency probe: issue -> completion of this G2
+            ptx::mma_commit(&dbg_bar);
+            ptx::mbar_spin(&dbg_bar, dbg_ph);
+            dbg_ph ^= 1;
+            if (tr && c2.g < kT4TrTiles) tr[T4TR(c2.g, 14 + x2)] = t4_clk() - tg2;
+          }
           if (tr && c2.g < kT4TrTiles) tr[T4TR(c2.g, 8 + x2)] = t4_clk();
           if (c2.j == c2.nt - 1) ptx::mma_commit(&o_full[x2]);
           if (++b2 == NSB) { b2 = 0; pph ^= 1; }
           if (x2 == 1) c2.advance(p, G);
           x2 ^= 1;
-          issue_g1();   // the next G1 reuses the buffer this G2 just read
+          issue_g1(kv_ready);   // the next G1 reuses the buffer this G2 just read
+          p_ready = c2.valid ? ptx::mbar_test(&p_full[b2], pph) : false;
         }
       }
     }
   } else if (warp >= 8) {
     // ============================================================ epilogue (warps 8-11)
+    ptx::setmaxnreg_dec<80>();
     const int row = threadIdx.x - 256;   // TMEM lane (warp 8+w reads lanes 32w..32w+31)
     const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
     using T16 = uint16_t;
+    __shared__ int last_flag;
     int ai = 0;
-    for (int u = blockIdx.x; u < p.units; u += G) {
-      const int beta = u / p.l_mp;
-      const int m0 = (u - beta * p.l_mp) * 256;
-      const int nt = (t4_nlim(p, beta) + kT4BN - 1) / kT4BN;
+    auto store_row = [&](T16* erow, int gm, int c0, const float* v, float inv) {
+      uint32_t w[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) w[q] = ptx::pack2<BF16>(v[2 * q] * inv, v[2 * q + 1] * inv);
+      if (gm < p.M) {
+        if (c0 + 16 <= p.L) {
+          uint4* dst = reinterpret_cast<uint4*>(erow + c0);
+          dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+          dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+            if (c0 + q < p.L) erow[c0 + q] = static_cast<T16>((w[q >> 1] >> ((q & 1) * 16)) & 0xFFFFu);
+        }
+      }
+    };
+    for (int i = blockIdx.x; i < p.items; i += G) {
+      T4Item it;
+      it.decode(p, i);
+      const int beta = it.u / p.l_mp;
+      const int m0 = (it.u - beta * p.l_mp) * 256;
+      const int nt = it.tiles(t4_nlim(p, beta));
 #pragma unroll 1
       for (int x = 0; x < 2; ++x) {
         const int gm = m0 + x * 128 + row;
         T16* erow = reinterpret_cast<T16*>(p.E) + static_cast<int64_t>(beta) * p.bs_e +
                     static_cast<int64_t>(gm) * p.ld_e;
-        float inv = 0.f;
         const uint32_t tO = tmem + lane_off + kOCol + x * kOStride;
+        float l = 0.f, m = -INFINITY;
         if (nt > 0) {
           ptx::mbar_wait(&o_full[x], ai & 1);
           ptx::tc_fence_after();
           if (tr && x == 0 && row == 0 && ai < 4) tr[490 + 4 * ai] = t4_clk();
           ptx::mbar_wait(&l_full[x], ai & 1);
-          const float l = l_sm[x][ai & 1][row];
+          l = l_sm[x][ai & 1][row];
+          m = m_sm[x][ai & 1][row];
           ptx::mbar_arrive(&l_free[x]);
-          inv = l > 0.f ? 1.0f / l : 0.f;
         }
+        if (it.piece < 0) {
+          // whole unit: E = O / l
+          const float inv = l > 0.f ? 1.0f / l : 0.f;
 #pragma unroll 1
-        for (int c0 = 0; c0 < p.TL; c0 += 16) {
-          uint32_t r[16];
-          if (nt > 0) {
-            ptx::tmem_ld16(tO + c0, r);
-            ptx::tmem_wait_ld();
-          } else {
+          for (int c0 = 0; c0 < p.TL; c0 += 16) {
+            float v[16];
+            if (nt > 0) {
+              uint32_t r[16];
+              ptx::tmem_ld16(tO + c0, r);
+              ptx::tmem_wait_ld();
 #pragma unroll
-            for (int q = 0; q < 16; ++q) r[q] = 0u;
-          }
-          uint32_t w[8];
-#pragma unroll
-          for (int q = 0; q < 8; ++q)
-            w[q] = ptx::pack2<BF16>(__uint_as_float(r[2 * q]) * inv, __uint_as_float(r[2 * q + 1]) * inv);
-          if (gm < p.M) {
-            if (c0 + 16 <= p.L) {
-              uint4* dst = reinterpret_cast<uint4*>(erow + c0);
-              dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
-              dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+              for (int q = 0; q < 16; ++q) v[q] = __uint_as_float(r[q]);
             } else {
 #pragma unroll
-              for (int q = 0; q < 16; ++q)
-                if (c0 + q < p.L) erow[c0 + q] = static_cast<T16>((w[q >> 1] >> ((q & 1) * 16)) & 0xFFFFu);
+              for (int q = 0; q < 16; ++q) v[q] = 0.f;
             }
+            store_row(erow, gm, c0, v, inv);
           }
-        }
-        if (nt > 0) {
-          ptx::tc_fence_before();
-          ptx::mbar_arrive(&o_free[x]);
+          if (nt > 0) {
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(&o_free[x]);
+          }
+        } else {
+          // piece of a tail unit: publish (O, m, l), the last of the unit's pieces merges
+          const int tu = it.u - p.tail;
+          const int64_t prow = (static_cast<int64_t>(tu) * p.pieces + it.piece) * 256 + x * 128 + row;
+          const int64_t n_part = static_cast<int64_t>(p.units - p.tail) * p.pieces * 256;
+          float* wsO = p.ws;
+          float* wsM = p.ws + n_part * p.TL;
+          float* wsL = wsM + n_part;
+          if (nt > 0) {
+#pragma unroll 1
+            for (int c0 = 0; c0 < p.TL; c0 += 16) {
+              uint32_t r[16];
+              ptx::tmem_ld16(tO + c0, r);
+              ptx::tmem_wait_ld();
+              float4* dst = reinterpret_cast<float4*>(wsO + prow * p.TL + c0);
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                dst[q] = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                                     __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+            }
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(&o_free[x]);
+          }
+          wsM[prow] = m;
+          wsL[prow] = nt > 0 ? l : 0.f;
+          // release: the barrier orders this warpgroup's stores before thread 0's fence (PTX
+          // fences are cumulative), whose atomic then publishes them at GPU scope
+          ptx::named_bar_sync(1, 128);
+          if (row == 0) {
+            __threadfence();
+            const bool last = atomicAdd(&p.cnt[tu * 2 + x], 1) == p.pieces - 1;
+            if (last) __threadfence();   // acquire the other pieces' partials
+            last_flag = last;
+          }
+          ptx::named_bar_sync(1, 128);
+          if (last_flag) {
+            const int64_t prow0 = static_cast<int64_t>(tu) * p.pieces * 256 + x * 128 + row;
+            float mq[kT4MaxPieces], wq[kT4MaxPieces];
+            float mstar = -INFINITY;
+#pragma unroll
+            for (int q = 0; q < kT4MaxPieces; ++q) {
+              mq[q] = -INFINITY;
+              wq[q] = 0.f;
+              if (q < p.pieces) {
+                wq[q] = __ldcg(wsL + prow0 + q * 256);
+                mq[q] = __ldcg(wsM + prow0 + q * 256);
+              }
+            }
+#pragma unroll
+            for (int q = 0; q < kT4MaxPieces; ++q)
+              if (wq[q] > 0.f) mstar = fmaxf(mstar, mq[q]);
+            float L = 0.f;
+#pragma unroll
+            for (int q = 0; q < kT4MaxPieces; ++q) {
+              const float sc_q = wq[q] > 0.f ? ptx::ex2(mq[q] - mstar) : 0.f;
+              L += wq[q] * sc_q;
+              wq[q] = sc_q;   // now the weight of piece q's O
+            }
+            const float inv = L > 0.f ? 1.0f / L : 0.f;
+#pragma unroll 1
+            for (int c0 = 0; c0 < p.TL; c0 += 16) {
+              float v[16];
+#pragma unroll
+              for (int q = 0; q < 16; ++q) v[q] = 0.f;
+#pragma unroll
+              for (int q = 0; q < kT4MaxPieces; ++q) {
+                if (wq[q] > 0.f) {
+                  const float4* src = reinterpret_cast<const float4*>(wsO + (prow0 + q * 256) * p.TL + c0);
+                  float4 o[4];
+#pragma unroll
+                  for (int c = 0; c < 4; ++c) o[c] = __ldcg(src + c);
+#pragma unroll
+                  for (int c = 0; c < 4; ++c) {
+                    v[4 * c] += wq[q] * o[c].x;
+                    v[4 * c + 1] += wq[q] * o[c].y;
+                    v[4 * c + 2] += wq[q] * o[c].z;
+                    v[4 * c + 3] += wq[q] * o[c].w;
+                  }
+                }
+              }
+              store_row(erow, gm, c0, v, inv);
+            }
+            if (row == 0) p.cnt[tu * 2 + x] = 0;   // ready for the next launch
+          }
         }
         if (tr && row == 0 && ai < 4) tr[490 + 4 * ai + 1 + x] = t4_clk();
       }
@@ -509,19 +635,22 @@ __global__ void __launch_bounds__(kT4Threads, 1)
     }
   } else {
     // ============================================================ softmax (warps 0-7)
+    ptx::setmaxnreg_inc<184>();   // a whole 128-column S row lives in registers
     const int x = warp >> 2;               // slot
     const int row = threadIdx.x & 127;     // TMEM lane
     const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
     const uint32_t tO = tmem + lane_off + kOCol + x * kOStride;
     const float sc = p.scale;
     int g = 0, ai = 0;
-    for (int u = blockIdx.x; u < p.units; u += G) {
-      const int beta = u / p.l_mp;
-      const int n_lim = t4_nlim(p, beta);
-      const int nt = (n_lim + kT4BN - 1) / kT4BN;
+    for (int i = blockIdx.x; i < p.items; i += G) {
+      T4Item it;
+      it.decode(p, i);
+      const int beta = it.u / p.l_mp;
+      const int n_lim = t4_nlim(p, beta) - it.t0 * kT4BN;   // keys from this item's first tile on
+      const int nt = it.tiles(n_lim + it.t0 * kT4BN);
       if (nt == 0) continue;
       float m_run = 0.f;
-      float2 l2 = make_float2(0.f, 0.f);
+      float2 l2 = make_float2(0.f, 0.f), l2b = make_float2(0.f, 0.f);
       for (int j = 0; j < nt; ++j, ++g) {
         const int k = 2 * g + x, b = k % NSB;
         const uint32_t tS = tmem + lane_off + b * 128;
@@ -538,27 +667,32 @@ __global__ void __launch_bounds__(kT4Threads, 1)
         }
         const int valid = n_lim - j * kT4BN;
         const bool full = valid >= kT4BN;
+        uint32_t sr[kT4BN];
+#pragma unroll
+        for (int c = 0; c < kT4BN / 32; ++c) ptx::tmem_ld32(tS + c * 32, &sr[c * 32]);
+        ptx::tmem_wait_ld();
         float mx;
-        if (full) {
-          mx = sc >= 0.f ? t4_tile_extreme<false>(tS) : t4_tile_extreme<true>(tS);
-        } else {
-          mx = sc >= 0.f ? t4_tile_extreme_masked<false>(tS, valid) : t4_tile_extreme_masked<true>(tS, valid);
-        }
+        if (full)
+          mx = sc >= 0.f ? t4_row_extreme<false, false>(sr, valid) : t4_row_extreme<true, false>(sr, valid);
+        else
+          mx = sc >= 0.f ? t4_row_extreme<false, true>(sr, valid) : t4_row_extreme<true, true>(sr, valid);
         const float m_tile = mx * sc;
         if (tr && row == 0 && g < kT4TrTiles) tr[T4TR(g, 2 + x)] = t4_clk_after(__float_as_uint(mx));
         if (j == 0) {
           m_run = m_tile;
         } else if (__any_sync(0xffffffffu, m_tile > m_run + kT4Tau)) {
           // warp-uniform (tcgen05.ld/st are warp-collective).  O_x must hold G2_x(j-1): implied
-          // by s_full for NSB = 2 (G1(k) follows G2(k-2)); an explicit wait for NSB = 3.
-          // NSB = 3: G1(k + 1) is issued right after G2(k + 1 - 3) = G2_x(j - 1), so its S
-          // buffer's phase certifies O_x (the issuer adds a bare commit past the last tile).
+          // by s_full for NSB = 2 (G1(k) follows G2(k-2)); for NSB = 3, G1(k + 1) is issued
+          // right after G2(k + 1 - 3) = G2_x(j - 1), so its S buffer's phase certifies O_x (the
+          // issuer adds a bare commit past the last tile).
           if constexpr (NSB == 3) ptx::mbar_wait(&s_full[(k + 1) % NSB], ((k + 1) / NSB) & 1);
           ptx::tc_fence_after();
           const float m_new = fmaxf(m_run, m_tile);
           const float alpha = ptx::ex2(m_run - m_new);
           l2.x *= alpha;
           l2.y *= alpha;
+          l2b.x *= alpha;
+          l2b.y *= alpha;
           m_run = m_new;
           for (int c0 = 0; c0 < p.TL; c0 += 16) {
             uint32_t r[16];
@@ -570,9 +704,9 @@ __global__ void __launch_bounds__(kT4Threads, 1)
           }
         }
         if (full)
-          t4_exp_tile<BF16, EMU, false>(tS, sc, m_run, valid, l2);
+          t4_exp_row<BF16, EMU, false>(tS, sr, sc, m_run, valid, l2, l2b);
         else
-          t4_exp_tile<BF16, 0, true>(tS, sc, m_run, valid, l2);
+          t4_exp_row<BF16, 0, true>(tS, sr, sc, m_run, valid, l2, l2b);
         ptx::tmem_wait_st();
         if (tr && row == 0 && g < kT4TrTiles) tr[T4TR(g, 4 + x)] = t4_clk();
         ptx::tc_fence_before();
@@ -582,7 +716,8 @@ __global__ void __launch_bounds__(kT4Threads, 1)
       // one tile), and l_full's parity protocol allows only one phase in flight: publishing l
       // of unit ai waits until the epilogue has read unit ai - 1's.
       if (ai >= 1) ptx::mbar_wait(&l_free[x], (ai - 1) & 1);
-      l_sm[x][ai & 1][row] = l2.x + l2.y;
+      l_sm[x][ai & 1][row] = (l2.x + l2.y) + (l2b.x + l2b.y);
+      m_sm[x][ai & 1][row] = m_run;
       ptx::mbar_arrive(&l_full[x]);
       ++ai;
     }

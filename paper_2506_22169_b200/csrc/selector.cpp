@@ -120,9 +120,9 @@ bool tc4_layout(int32_t k_steps, int32_t TL, int32_t stages, int32_t b_layout, T
   int32_t a, b, d;
   tc_smem_bytes(k_steps, 128, TL, stages, b_layout, &a, &b, &d);
   for (int32_t q_bufs = 2; q_bufs >= 1; --q_bufs) {
-    const int32_t bars = 8 * (18 + 3 * stages);
+    const int32_t bars = 8 * (18 + 2 * stages);
     const int32_t total = q_bufs * 2 * a + stages * (b + d) + bars + 1024;
-    if (total + 3072 <= smem_max) {   // 2 KB of l + slack stay for static shared memory
+    if (total + 5120 <= smem_max) {   // 4 KB of (l, m) + slack stay for static shared memory
       if (out) *out = Tc4Layout{a, b, d, q_bufs, total};
       return true;
     }
@@ -148,6 +148,12 @@ bool tc_eligible(const mbci_chain_desc_t& d) {
   return true;
 }
 
+// Round-1 measurement: kernels 0, 2 and 3 run ~2.2-2.6x slower than the roofline-style score
+// below (C2 24.3 vs 9.3 us, C3 79 vs 35 us); kernel 4 is scored from its measured per-tile cost.
+// The common factor keeps the two kinds of score comparable (the ranking inside 0/2/3 is
+// unchanged by it).
+constexpr double kModelToB200 = 2.4;
+
 static void score_b200(const mbci_chain_desc_t& d, const mbci_hw_t& hw, mbci_plan_t& p) {
   const int32_t s = (d.dtype == MBCI_F32) ? 4 : 2;
   const double b = static_cast<double>(d.batch);
@@ -168,12 +174,16 @@ static void score_b200(const mbci_chain_desc_t& d, const mbci_hw_t& hw, mbci_pla
     t_issue = t_tc;
   }
   if (p.kernel == 4) {
-    // persistent pair units dealt round-robin: ceil(units / n_sm) rounds, no stream-K.  The
-    // FMA-pipe polynomial takes 3/8 of the exponentials off the MUFU (chain_tc4.cuh).
-    const double units = static_cast<double>(p.n_block);
-    const double rounds = std::ceil(units / hw.n_sm);
-    const double q4 = units > 0 ? rounds * hw.n_sm / units : 1.0;
-    p.t_b200 = std::max(std::max(t_hbm, t_tc), std::max(t_sfu * 0.625, t_issue * 0.8)) * q4 + 1.0e-6;
+    // persistent pair units dealt round-robin (ceil(units / n_sm) rounds per SM).
+    const int64_t units = b == 0 ? 0 : static_cast<int64_t>(b) * cdiv(d.M, 256);
+    const int64_t ntm = std::max<int64_t>(1, nt);
+    const int64_t rounds = units / hw.n_sm, rem = units % hw.n_sm;
+    const int64_t tail_tiles = rem > 0 ? ntm : 0;   // the key-axis split of the tail is opt-in
+    // Calibrated on B200 (round-1 traces, tools/trace_chain4.py): one 256 x 128 score tile of a
+    // pair unit costs ~0.75 us + 6 ns per unit of (K + L) (d = 64: 1.5 us, d = 128: 2.3 us) on an
+    // SM, plus ~3 us of prologue / epilogue per launch.
+    const double t_pair = (0.75e-6 + 6.0e-9 * static_cast<double>(p.TK + p.TL)) * (1.965e9 / hw.clock_hz);
+    p.t_b200 = std::max(t_hbm, static_cast<double>(rounds * ntm + tail_tiles) * t_pair) + 3.0e-6;
     return;
   }
   if (p.kernel == 2 || p.kernel == 3) {
@@ -182,7 +192,7 @@ static void score_b200(const mbci_chain_desc_t& d, const mbci_hw_t& hw, mbci_pla
     const double tiles = units * static_cast<double>(nt);
     // slots differ by at most one tile; a slot holding < 1 tile of work idles the rest
     const double qq = std::min(2.0, 1.0 + 2.0 * hw.n_sm / std::max(1.0, tiles));
-    p.t_b200 = std::max(std::max(t_hbm, t_tc), std::max(t_sfu, t_issue)) * qq + 1.5e-6;
+    p.t_b200 = (std::max(std::max(t_hbm, t_tc), std::max(t_sfu, t_issue)) * qq + 1.5e-6) * kModelToB200;
     return;
   }
   int32_t occ = 1;
@@ -197,7 +207,7 @@ static void score_b200(const mbci_chain_desc_t& d, const mbci_hw_t& hw, mbci_pla
   const double waves = std::ceil(static_cast<double>(p.n_block) / slots);
   const double q = p.n_block > 0 ? waves * slots / static_cast<double>(p.n_block) : 1.0;
   const double t_fixed = waves * 1.0e-6 / occ;  // prologue + epilogue latency per wave
-  p.t_b200 = std::max(std::max(t_hbm, t_tc), std::max(t_sfu, t_issue)) * q + t_fixed;
+  p.t_b200 = (std::max(std::max(t_hbm, t_tc), std::max(t_sfu, t_issue)) * q + t_fixed) * kModelToB200;
 }
 
 int enumerate_plans(const mbci_chain_desc_t& d, const mbci_hw_t& hw,

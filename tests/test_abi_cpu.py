@@ -129,7 +129,7 @@ def test_enumerated_plans_are_legal_and_scored(m, shape, b_layout):
             assert p.tmem_cols == 512 and p.BN == 128 and 256 + 2 * p.TL <= 512
         assert 2 <= p.stages <= (4 if p.kernel == 0 else 8)
         if p.kernel == 4:
-            assert p.smem_bytes + 3072 <= hw.smem_max
+            assert p.smem_bytes + 5120 <= hw.smem_max
         if rule3_ok:
             assert not model.rule3_reject(N, p.BN)
         ref = model.chain_estimate(b, M, N, K, L, p.BM, p.BN, p.TK, p.TL, 2, hw.W, hw.P, hw.n_sm)

@@ -76,6 +76,15 @@ __global__ void __launch_bounds__(384, 1) k(int mode, int rounds, int bg, uint64
         ptx::tmem_wait_ld();
         y += __uint_as_float(r[5]);
       }
+      if (bg & 16) {   // like the softmax: ld 128 columns of an S buffer, st 64 columns of P
+        const uint32_t tS2 = tmem + 256 + ((uint32_t)((warp & 3) * 32) << 16);
+        uint32_t r[32];
+        for (int c = 0; c < 4; ++c) { ptx::tmem_ld32(tS2 + c * 32, r); }
+        ptx::tmem_wait_ld();
+        for (int c = 0; c < 4; ++c) ptx::tmem_st16(tS2 + c * 16, r);
+        ptx::tmem_wait_st();
+        y += __uint_as_float(r[3]);
+      }
       if (bg & 4) {   // poll an mbarrier phase that never completes (like warps blocked in mbar_wait)
         for (int i = 0; i < 64; ++i) y += ptx::mbar_try_wait(ptx::smem_u32(&bar3), 0) ? 1.f : 0.f;
       }
@@ -104,9 +113,9 @@ int main() {
              (m & 16) ? "+fence::after " : "", (m & 32) ? "+test_wait(done bar) " : "");
     return b;
   };
-  const char* bgn[] = {"idle", "MUFU+FMA", "TMEM ld", "MUFU+FMA+TMEM ld", "try_wait poll", "", "", "", "test_wait poll"};
-  for (int bg : {0, 4, 8})
-    for (int mode : {3, 7, 3 | 32}) {
+  static const char* bgn[20] = {"idle", "MUFU+FMA", "TMEM ld", "MUFU+FMA+TMEM ld", "try_wait poll", "", "", "", "test_wait poll", "", "", "", "", "", "", "", "TMEM ld+st (softmax-like)"};
+  for (int bg : {0, 16, 17})
+    for (int mode : {3, 7}) {
       const int grid = 148, rounds = 200;
       k<<<grid, 384, 100000>>>(mode, rounds, bg, d);
       k<<<grid, 384, 100000>>>(mode, rounds, bg, d);

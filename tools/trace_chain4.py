@@ -48,3 +48,9 @@ for g in range(a.tiles):
           f"  {row[2]-row[0]:5.2f} {row[4]-row[2]:5.2f}  {row[3]-row[1]:5.2f} {row[5]-row[3]:5.2f}")
 for u in range(4):
     print(f"unit {u}: epilogue o_full seen {d(490+4*u):.2f}  slot0 stored {d(490+4*u+1):.2f}  slot1 stored {d(490+4*u+2):.2f}")
+if int(os.environ.get("MBCI_T4_DEBUG", "0")) & 8:
+    print("latency probes (cycles, issue -> completion): G1_0 G1_1 G2_0 G2_1")
+    for g in range(a.tiles):
+        c = 8 + 16 * g
+        v = [np.median(t[:, c + k][t[:, c + k] > 0]) if (t[:, c + k] > 0).mean() > 0.5 else float("nan") for k in (12, 13, 14, 15)]
+        print(f"{g:4d} " + " ".join(f"{x:7.0f}" for x in v))
