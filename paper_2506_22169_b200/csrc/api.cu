@@ -355,8 +355,8 @@ mbci_status_t setup_plan(mbci_chain* h) {
   } else if (p.kernel == 4) {
     const int32_t k_steps = static_cast<int32_t>((d.K + 15) / 16);
     Tc4Layout lay;
-    if (d.op != MBCI_OP_SOFTMAX || k_steps < 1 || d.N < 1 || !tc4_layout(k_steps, p.TL, p.stages, d.b_layout, &lay))
-      return fail(MBCI_ERR_UNSUPPORTED, "kernel-4 plan needs softmax, K, N >= 1 and must fit SMEM/TMEM");
+    if (k_steps < 1 || d.N < 1 || !tc4_layout(k_steps, p.TL, p.stages, d.b_layout, &lay))
+      return fail(MBCI_ERR_UNSUPPORTED, "kernel-4 plan needs K, N >= 1 and must fit SMEM/TMEM");
     p.smem_bytes = lay.smem_total;
     p.tmem_cols = 512;
     h->kch = std::max(1, (16 * k_steps + 63) / 64);
@@ -374,7 +374,8 @@ mbci_status_t setup_plan(mbci_chain* h) {
     t.k_steps = k_steps;
     t.stages = p.stages;
     t.q_bufs = lay.q_bufs;
-    t.scale = d.scale * 1.4426950408889634f;
+    t.op = d.op;
+    t.scale = d.op == MBCI_OP_SOFTMAX ? d.scale * 1.4426950408889634f : (d.op == MBCI_OP_SCALE ? d.scale : 1.0f);
     t.ld_e = d.ld_e;
     t.bs_e = d.bs_e;
     if (const char* dbg = getenv("MBCI_T4_DEBUG")) t.dbg = atoi(dbg);

@@ -1,8 +1,9 @@
-// chain_tc4.cuh — persistent ping-pong attention chain E = softmax(s·A·B)·D on sm_100a.
+// chain_tc4.cuh — persistent ping-pong fused chain E = op(A·B)·D on sm_100a.
 //
-// Same arithmetic as chain_tc.cuh for op = SOFTMAX (mbci.h; PAPER.md:196 chain, :498 softmax
-// between the GEMMs, :489 batched layout); a different layout of the work, built for the MUFU
-// (ex2) + tensor-core balance of d <= 128 attention on B200:
+// Same arithmetic as chain_tc.cuh (mbci.h; PAPER.md:196 chain, :498 softmax between the GEMMs,
+// :489 batched layout); a different layout of the work, built for the MUFU (ex2) + tensor-core
+// balance of d <= 128 attention on B200 (op = SOFTMAX) and reused for the plain chains (NONE /
+// SCALE: the warpgroups only convert S to 16-bit P):
 //
 // * Persistent grid (one CTA per SM).  A unit is (β, a PAIR of 128-row m-tiles) — the paper's
 //   spatial loop m bound to CTAs (Rule 1) with the whole L in the CTA (the h loop
@@ -50,7 +51,8 @@ struct Tc4Params {
   int32_t k_steps;         // ceil(K / 16) >= 1
   int32_t stages;          // K/V ring depth
   int32_t q_bufs;          // Q-pair buffers (1 or 2)
-  float scale;             // softmax scale * log2(e)
+  int32_t op;              // 2 softmax; 1 scale, 0 none (P = cvt(scale * S), E = O)
+  float scale;             // softmax: scale * log2(e); SCALE: the multiplier; NONE: 1
   const int32_t* valid_len;
   void* E;
   int64_t ld_e, bs_e;
@@ -198,6 +200,24 @@ __device__ __forceinline__ void t4_exp_row(uint32_t tS, const uint32_t (&sr)[kT4
       }
       if (c & 1) l2b = __fadd2_rn(l2b, e); else l2a = __fadd2_rn(l2a, e);
       pk[c] = ptx::pack2<BF16>(e.x, e.y);
+    }
+    ptx::tmem_st16(tS + ch * 16, pk);
+  }
+}
+
+// NONE / SCALE: P = cvt(scale * S) for the 128 scores of the row, written as 16-bit P into TMEM
+// columns [0, 64) of the S buffer (no max, no exponentials, no row sum).
+template <bool BF16>
+__device__ __forceinline__ void t4_cvt_row(uint32_t tS, const uint32_t (&sr)[kT4BN], float sc) {
+  const float2 sc2 = make_float2(sc, sc);
+#pragma unroll
+  for (int ch = 0; ch < 4; ++ch) {
+    uint32_t pk[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+      const int cp = ch * 16 + c;
+      const float2 z = __fmul2_rn(make_float2(__uint_as_float(sr[2 * cp]), __uint_as_float(sr[2 * cp + 1])), sc2);
+      pk[c] = ptx::pack2<BF16>(z.x, z.y);
     }
     ptx::tmem_st16(tS + ch * 16, pk);
   }
@@ -671,6 +691,14 @@ __global__ void __launch_bounds__(kT4Threads, 1)
 #pragma unroll
         for (int c = 0; c < kT4BN / 32; ++c) ptx::tmem_ld32(tS + c * 32, &sr[c * 32]);
         ptx::tmem_wait_ld();
+        if (p.op != 2) {
+          // NONE / SCALE: padded keys have S = 0 and zero V rows (TMA fill), no masking needed
+          t4_cvt_row<BF16>(tS, sr, sc);
+          ptx::tmem_wait_st();
+          ptx::tc_fence_before();
+          ptx::mbar_arrive(&p_full[b]);
+          continue;
+        }
         float mx;
         if (full)
           mx = sc >= 0.f ? t4_row_extreme<false, false>(sr, valid) : t4_row_extreme<true, false>(sr, valid);
@@ -716,7 +744,7 @@ __global__ void __launch_bounds__(kT4Threads, 1)
       // one tile), and l_full's parity protocol allows only one phase in flight: publishing l
       // of unit ai waits until the epilogue has read unit ai - 1's.
       if (ai >= 1) ptx::mbar_wait(&l_free[x], (ai - 1) & 1);
-      l_sm[x][ai & 1][row] = (l2.x + l2.y) + (l2b.x + l2b.y);
+      l_sm[x][ai & 1][row] = p.op == 2 ? (l2.x + l2.y) + (l2b.x + l2b.y) : 1.0f;   // E = O / l
       m_sm[x][ai & 1][row] = m_run;
       ptx::mbar_arrive(&l_full[x]);
       ++ai;

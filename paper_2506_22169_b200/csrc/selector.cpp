@@ -182,7 +182,10 @@ static void score_b200(const mbci_chain_desc_t& d, const mbci_hw_t& hw, mbci_pla
     // Calibrated on B200 (round-1 traces, tools/trace_chain4.py): one 256 x 128 score tile of a
     // pair unit costs ~0.75 us + 6 ns per unit of (K + L) (d = 64: 1.5 us, d = 128: 2.3 us) on an
     // SM, plus ~3 us of prologue / epilogue per launch.
-    const double t_pair = (0.75e-6 + 6.0e-9 * static_cast<double>(p.TK + p.TL)) * (1.965e9 / hw.clock_hz);
+    // NONE / SCALE (no exponentials): the issuer and tensor pipe bound the tile, ~half the cost.
+    const double t_pair = (d.op == MBCI_OP_SOFTMAX ? 0.75e-6 + 6.0e-9 * static_cast<double>(p.TK + p.TL)
+                                                   : 0.15e-6 + 4.0e-9 * static_cast<double>(p.TK + p.TL)) *
+                          (1.965e9 / hw.clock_hz);
     p.t_b200 = std::max(t_hbm, static_cast<double>(rounds * ntm + tail_tiles) * t_pair) + 3.0e-6;
     return;
   }
@@ -224,7 +227,7 @@ int enumerate_plans(const mbci_chain_desc_t& d, const mbci_hw_t& hw,
         for (int32_t TL = 16; TL <= lpad; TL += 16) {
           if (apply_rule3 && d.L > 0 && rule3_reject(d.L, TL)) continue;
           if (2 * BN + TL > hw.tmem_cols) continue;  // TMEM budget
-          for (int32_t st = 2; st <= 8 && BN == 128 && TL == lpad && d.op == MBCI_OP_SOFTMAX && k_steps >= 1 &&
+          for (int32_t st = 2; st <= 8 && BN == 128 && TL == lpad && k_steps >= 1 &&
                                d.N >= 1; ++st) {
             Tc4Layout lay4;
             if (tc4_layout(k_steps, TL, st, d.b_layout, &lay4, hw.smem_max)) {

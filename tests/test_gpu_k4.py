@@ -18,7 +18,7 @@ import torch
 
 import mbci_inputs as gen
 import oracle
-from gpu_helpers import e_f64, run_chain, to_dev
+from gpu_helpers import e_bits, e_f64, rn_bits, run_chain, to_dev
 
 pytestmark = pytest.mark.gpu
 
@@ -188,3 +188,37 @@ def test_k4_strided_operands(mbci):
     assert np.all(np.isnan(Ef[0, M * ldE:]))
     assert np.all(np.isnan(Ef[0, :ldE * M].reshape(M, ldE)[:, L:]))
     assert oracle.row_max_error(got, oracle.chain(inp, "softmax", 0.125)) <= BUDGET["f16"]
+
+
+# ------------------------------------------------------------------ NONE / SCALE on kernel 4
+@pytest.mark.parametrize("dtype,K", [("f16", 16), ("f16", 64), ("bf16", 32), ("bf16", 128), ("f16", 128)])
+@pytest.mark.parametrize("b_layout", [0, 1])
+def test_k4_plain_chain_integer_bitwise(mbci, dtype, K, b_layout):
+    """Integers in [-2, 2]: every product and fp32 partial sum is exact, so E must equal
+    RN-even(oracle E) bit for bit (SURVEY §8(c) pin), for NONE and SCALE (0.5)."""
+    inp = gen.make_chain_inputs(200 + K, dtype, 3, 384, 640, K, K, b_layout, kind="int")
+    for op, sc in (("none", 1.0), ("scale", 0.5)):
+        E, ch = run_chain(mbci, inp, op, sc, plan=k4_plan(mbci, K))
+        assert ch.plan().kernel == 4, ch.describe()
+        ref = oracle.chain(inp, op, sc)
+        assert np.array_equal(e_bits(E), rn_bits(ref, dtype)), ch.describe()
+
+
+@pytest.mark.parametrize("M,N,K,L", [(300, 333, 48, 40), (129, 1000, 72, 56), (1, 1, 16, 16)])
+def test_k4_plain_chain_ragged(mbci, M, N, K, L):
+    sig = (1.0, 1.0 / math.sqrt(K), 1.0 / math.sqrt(N))
+    inp = gen.make_chain_inputs(M + N + 7, "bf16", 2, M, N, K, L, 1, sigmas=sig)
+    for op, sc in (("none", 1.0), ("scale", -0.75)):
+        E, ch = run_chain(mbci, inp, op, sc, plan=k4_plan(mbci, L))
+        err = oracle.row_max_error(e_f64(E, "bf16"), oracle.chain(inp, op, sc))
+        assert err <= BUDGET["bf16"], (op, err, ch.describe())
+
+
+def test_k4_plain_chain_C4_shape_sampled(mbci):
+    b, M, N, K = 64, 2048, 2048, 64
+    inp = gen.make_chain_inputs(0, "bf16", b, M, N, K, K, 0, sigmas=(1.0, 1.0 / math.sqrt(K), 1.0 / math.sqrt(N)))
+    E, ch = run_chain(mbci, inp, "none", 1.0, plan=k4_plan(mbci, K))
+    rows = np.stack([np.arange(b), (np.arange(b) * 389) % M], axis=1).astype(np.int64)
+    ref = oracle.chain(inp, "none", 1.0, rows=rows)
+    err = oracle.row_max_error(e_f64(E, "bf16")[rows[:, 0], rows[:, 1]], ref)
+    assert err <= BUDGET["bf16"], (err, ch.describe())

@@ -1,8 +1,6 @@
 #!/bin/bash
-# quick kernel-4 check: parity suite, then C2 / C3 timings with and without the tail split
+# quick kernel-4 check: parity suite, bench (graph-timed) for the softmax and plain configs
 timeout 900 python -m pytest tests/test_gpu_k4.py -q -x 2>&1 | tail -2
-for ns in "" 1; do
-  MBCI_T4_NO_SPLIT=$ns timeout 60 python tools/run_plan.py --plan 4:128:64:3 --iters 50 2>&1 | tail -1
-  MBCI_T4_NO_SPLIT=$ns timeout 60 python tools/run_plan.py --plan 4:128:64:3 --shape 128,1024,1024,64,64 --dtype bf16 --iters 20 2>&1 | tail -1
+for c in C2 C3 C6 C4-16 C4-64 C4-128; do
+  timeout 300 python bench.py --config $c --steps 50 --warmup 5 --no-cpu-baseline --sustain 0.2 | python -c "import sys,json; j=json.loads(sys.stdin.read()); print(j['config']['name'], round(j['value'],1), 'GB/s', round(j['us_per_chain'],2), 'us', j['config']['plan'][:60])"
 done
-MBCI_LIB=trace timeout 120 python tools/trace_chain4.py --plan 4:128:64:3 --tiles 8
