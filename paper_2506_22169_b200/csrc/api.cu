@@ -151,8 +151,11 @@ using Tc4Kernel = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, Tc4Params);
 template <bool BF16, int KCH, int BL, int DCH>
 Tc4Kernel pick4_emu(int emu) {
   constexpr int NSB = DCH == 1 ? 3 : 2;   // three S buffers fit TMEM next to two 64-column O
-  return emu == 0 ? (Tc4Kernel)k_chain_tc4<BF16, KCH, BL, DCH, 0, NSB>
-                  : (Tc4Kernel)k_chain_tc4<BF16, KCH, BL, DCH, 3, NSB>;
+  switch (emu) {
+    case 0: return (Tc4Kernel)k_chain_tc4<BF16, KCH, BL, DCH, 0, NSB>;
+    case 2: return (Tc4Kernel)k_chain_tc4<BF16, KCH, BL, DCH, 2, NSB>;
+    default: return (Tc4Kernel)k_chain_tc4<BF16, KCH, BL, DCH, 3, NSB>;
+  }
 }
 template <bool BF16, int KCH, int BL>
 Tc4Kernel pick4_d(int dch, int emu) {
@@ -171,8 +174,8 @@ Tc4Kernel pick_tc4(bool bf16, int kch, int bl, int dch, int emu) {
 // (MBCI_T4_EMU overrides; 0 = all on the MUFU).
 int t4_emu_default() {
   const char* e = getenv("MBCI_T4_EMU");
-  if (e && (e[0] == '0' || e[0] == '3')) return e[0] - '0';
-  return 3;
+  if (e && (e[0] == '0' || e[0] == '2' || e[0] == '3')) return e[0] - '0';
+  return 2;   // 2/8 of the pairs: C2 21.0 us, C3 61.7 (3/8: 21.5, 63.1; 0: 22.2, 65.4; 4/8 slower)
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;

@@ -22,7 +22,7 @@
 //   of the S buffer it came from.  tcgen05 ops of one thread complete in issue order, so a G1
 //   rewrites a buffer only after the G2 that read its P.
 // * Exponentials: z = s·log2(e)·S − m with packed f32x2 FMA; p = 2^z on the MUFU (ex2.approx)
-//   or, for EMU of every 8 column pairs, on the FMA pipe (Cody–Waite split + degree-3 minimax
+//   or, for EMU of every 8 column pairs (default 2, MBCI_T4_EMU), on the FMA pipe (Cody–Waite split + degree-3 minimax
 //   polynomial, max rel. error 8.8e-5 < the 16-bit P rounding) so both pipes share the work.
 //   Lazy rescale: the running max only moves when a tile's max exceeds it by > τ = 8 (log2),
 //   exact in real arithmetic (R4).

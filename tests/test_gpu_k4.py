@@ -33,7 +33,7 @@ def mbci():
     return m
 
 
-@pytest.fixture(params=["0", "3"], ids=["mufu", "poly3of8"])
+@pytest.fixture(params=["0", "2", "3"], ids=["mufu", "poly2of8", "poly3of8"])
 def emu(request, monkeypatch):
     monkeypatch.setenv("MBCI_T4_EMU", request.param)
     return request.param
