@@ -391,43 +391,20 @@ mbci_status_t setup_plan(mbci_chain* h) {
     t.idesc2 = ptx::idesc_f16(fmt, 0, 1u, 128, (uint32_t)p.TL);
     int n_sm = 148;
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, h->device);
-    // Wave quantisation: the last, partial round of units is cut along the key axis so that it
-    // fills the SMs (kernel 4); pieces are merged by log-sum-exp in the kernel.
+    // Wave quantisation: when the last, partial round has r <= n_sm / 2 units, each becomes two
+    // "half" items (one 128-row Q tile, keys split between the two slots, merged in the CTA),
+    // so the round takes half the tiles (chain_tc4.cuh).  Needs no key padding and an even
+    // tile count; MBCI_T4_NO_HALF=1 disables it.
     t.nt_max = (int32_t)((d.N + 127) / 128);
     const int64_t rounds = units / n_sm, rem = units % n_sm;
-    int32_t pieces = 1;
-    // Opt-in (MBCI_T4_SPLIT=1) until the merge is cheaper: on C2 the split saves tile-time but
-    // its fence + atomic + L2 round trips cost more (bench: 30.6 us split vs 20.3 us unsplit).
-    const char* split_env = getenv("MBCI_T4_SPLIT");
-    if (rem > 0 && t.nt_max > 1 && split_env && split_env[0] == '1') {
-      const int64_t fmax = std::min<int64_t>(std::min<int64_t>(t.nt_max, n_sm / rem), kT4MaxPieces);
-      int64_t best = t.nt_max;
-      for (int64_t f = 2; f <= fmax; ++f) {
-        const int64_t c = (t.nt_max + f - 1) / f;
-        if (c < best) { best = c; pieces = (int32_t)f; }
-      }
-    }
-    t.pieces = pieces;
-    t.piece_tiles = (t.nt_max + pieces - 1) / pieces;
-    t.tail = pieces > 1 ? (int32_t)(rounds * n_sm) : (int32_t)units;
-    t.items = (int32_t)(t.tail + (units - t.tail) * pieces);
+    // (the two ring entries per step need stages >= 4 with three S buffers, >= 3 with two)
+    const char* no_half = getenv("MBCI_T4_NO_HALF");
+    const bool halves = rem > 0 && 2 * rem <= n_sm && t.nt_max % 2 == 0 && d.mask == MBCI_MASK_NONE &&
+                        p.stages >= (h->dch == 1 ? 4 : 3) && !(no_half && no_half[0] == '1');
+    t.half_from = halves ? (int32_t)(rounds * n_sm) : (int32_t)units;
+    t.items = (int32_t)(halves ? t.half_from + 2 * rem : units);
     h->grid2 = (int32_t)std::max<int64_t>(1, std::min<int64_t>(n_sm, t.items));
     p.n_block = t.items;
-    if (pieces > 1) {
-      const int64_t part_rows = (units - t.tail) * pieces * 256;
-      const size_t need = (size_t)part_rows * (p.TL + 2) * 4 + (size_t)(units - t.tail) * 2 * 4;
-      if (h->ws2_bytes < need) {
-        if (h->ws2) cudaFree(h->ws2);
-        h->ws2 = nullptr;
-        h->ws2_bytes = 0;
-        if (cudaMalloc(&h->ws2, need) != cudaSuccess) return fail(MBCI_ERR_NOMEM, "kernel-4 merge workspace");
-        h->ws2_bytes = need;
-      }
-      cudaError_t me = cudaMemset(h->ws2, 0, need);
-      if (me != cudaSuccess) return cuda_fail(me, "workspace memset");
-      t.ws = static_cast<float*>(h->ws2);
-      t.cnt = reinterpret_cast<int32_t*>(static_cast<float*>(h->ws2) + (size_t)part_rows * (p.TL + 2));
-    }
     cudaError_t e = cudaFuncSetAttribute((const void*)h->tc4, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          p.smem_bytes);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");

@@ -59,13 +59,12 @@ struct Tc4Params {
   uint32_t q_bytes;        // one 128-row Q tile
   uint32_t b_stage_bytes, d_stage_bytes, kp_rows;
   uint32_t idesc1, idesc2;
-  // Work items (one per CTA round): items [0, tail) are whole pair units; the last r = units -
-  // tail units are cut along the key axis into `pieces` items of `piece_tiles` 128-key tiles,
-  // so the final round fills the SMs (wave quantisation).  Each piece stores its partial
-  // (O, m, l) to `ws`; the last piece to finish (atomic count in `cnt`) merges them.
-  int32_t items, tail, pieces, piece_tiles, nt_max;
-  float* ws;               // [r * pieces][256][TL] O, then m [r * pieces][256], l [r * pieces][256]
-  int32_t* cnt;            // [r][2], zero between launches
+  // Work items (one per CTA round): items [0, half_from) are whole pair units (item = unit).
+  // When the last, partial round would leave SMs idle, its r units become 2r "half" items
+  // [half_from, items): one 128-row Q tile each, whose two slots split the key tiles (slot x
+  // takes tiles [x·h, x·h + h), h = nt_max / 2) and whose epilogue merges the two partial
+  // (O, m, l) rows inside the CTA (log-sum-exp).  Only without key padding and with nt_max even.
+  int32_t items, half_from, nt_max;
   uint64_t* trace;         // [gridDim.x][kT4TraceSlots] (MBCI_TRACE builds only)
   int32_t dbg;             // diagnostics only (MBCI_T4_DEBUG): 1 = softmax skips its TMEM/math work,
                            // 2 = issuer skips the G2 MMAs, 4 = issuer skips the G1 MMAs
@@ -74,7 +73,6 @@ struct Tc4Params {
 constexpr int kT4Threads = 512;
 constexpr int kT4BN = 128;
 constexpr float kT4Tau = 8.0f;
-constexpr int kT4MaxPieces = 4;   // key-axis pieces per tail unit (api.cu caps the split)
 constexpr int kT4TraceSlots = 512;
 // trace layout per CTA (MBCI_TRACE builds): [0] start (globaltimer ns) [1] setup [2] smid [3] end,
 // [4] clock64 at start; per flat tile g < 40 and slot x, SM clock64 at 8 + 12*g + {0+x: S ready,
@@ -100,26 +98,30 @@ __device__ __forceinline__ int t4_nlim(const Tc4Params& p, int beta) {
   return n;
 }
 
-// Work item i -> pair unit u, its key-tile range [t0, t1) and piece index (-1: whole unit).
+// Work item i -> pair unit u and, for a half item, which 128-row Q tile of it (see Tc4Params).
 struct T4Item {
-  int u, t0, t1, piece;
+  int u, half;   // pair unit; -1: the whole unit, 0 / 1: which 128-row tile of it (half item)
   __device__ __forceinline__ void decode(const Tc4Params& p, int i) {
-    if (i < p.tail) {
-      u = i; t0 = 0; t1 = p.nt_max; piece = -1;
+    if (i < p.half_from) {
+      u = i;
+      half = -1;
     } else {
-      const int q = i - p.tail;
-      u = p.tail + q / p.pieces;
-      piece = q - (u - p.tail) * p.pieces;
-      t0 = piece * p.piece_tiles;
-      t1 = min(t0 + p.piece_tiles, p.nt_max);
+      const int q = i - p.half_from;
+      u = p.half_from + (q >> 1);
+      half = q & 1;
     }
   }
-  // valid tiles of this item given the unit's key limit
+  // steps (K/V tiles per slot) of this item given the unit's key limit; a half item's two
+  // slots take half of the (unmasked, even) tile count each
   __device__ __forceinline__ int tiles(int n_lim) const {
     const int ntv = (n_lim + kT4BN - 1) / kT4BN;
-    return max(0, min(t1, ntv) - t0);
+    return half < 0 ? ntv : ntv / 2;
   }
 };
+
+__device__ __forceinline__ void t4_next_entry(int& st, uint32_t& ph, int S) {
+  if (++st == S) { st = 0; ph ^= 1; }
+}
 
 // 2^x for a pair, on the FMA/ALU pipes.  x <= 2^22; results below 2^-127 flush towards 0.
 //   x = n + f, n = floor(x) (round-down add of 1.5·2^23), f in [0, 1);
@@ -228,8 +230,9 @@ __device__ __forceinline__ void t4_cvt_row(uint32_t tS, const uint32_t (&sr)[kT4
 // qph) and active-unit index ai, and the K/V ring stage (st, parity sph) of the tile.  Per tile
 // the issuer only increments counters; divisions happen once per unit.
 struct T4Cursor {
-  int i, u, t0, nt, j, ai, qb, qph, st, sph, g;
-  bool valid;
+  int i, u, nt, j, ai, qb, qph, st, g;
+  uint32_t sph;
+  bool valid, hf;   // hf: half item (two K/V ring entries per step, one per slot)
   __device__ __forceinline__ void skip(const Tc4Params& p, int G) {
     while (i < p.items) {
       T4Item it;
@@ -237,7 +240,7 @@ struct T4Cursor {
       nt = it.tiles(t4_nlim(p, it.u / p.l_mp));
       if (nt > 0) {
         u = it.u;
-        t0 = it.t0;
+        hf = it.half >= 0;
         return;
       }
       i += G;
@@ -245,12 +248,19 @@ struct T4Cursor {
     valid = false;
   }
   __device__ __forceinline__ void init(const Tc4Params& p, int G) {
-    i = blockIdx.x; j = 0; ai = 0; qb = 0; qph = 0; st = 0; sph = 0; g = 0; valid = true; nt = 0;
+    i = blockIdx.x; j = 0; ai = 0; qb = 0; qph = 0; st = 0; sph = 0; g = 0; valid = true; nt = 0; hf = false;
     skip(p, G);
+  }
+  // ring entry (stage, parity) of slot x in the current step
+  __device__ __forceinline__ void entry(int x, int S, int& s, uint32_t& ph) const {
+    s = st;
+    ph = sph;
+    if (hf && x == 1) t4_next_entry(s, ph, S);
   }
   __device__ __forceinline__ void advance(const Tc4Params& p, int G) {
     ++g;
-    if (++st == p.stages) { st = 0; sph ^= 1; }
+    t4_next_entry(st, sph, p.stages);
+    if (hf) t4_next_entry(st, sph, p.stages);
     if (++j >= nt) {
       j = 0;
       ++ai;
@@ -266,9 +276,11 @@ struct T4Cursor {
 //   NSB = 3 (TL <= 64): three 128-column S buffers + two 64-column O; G1(k+3) follows G2(k), so
 //   a slot's next S tile is computed while its softmax still runs (the softmax warpgroups never
 //   wait for G2 + G1 latency), and the lazy rescale waits for G2_x(j-1) via S(k+1)'s phase.
-// Commits are the scarce resource of the issuer (tools/commit_bench.cu: each tcgen05.commit
-// occupies the tensor pipe ~220 cycles): per slot-tile one (s_full), plus o_full per unit and
-// slot and q_empty per unit; everything else is inferred from those phases.
+// Commits (each ~170 cycles of issuer time, tools/sync_cost_bench.cu): per slot-tile one
+// (s_full), per step one K/V release (two for a half item), plus o_full per item and slot and
+// q_empty per item.
+// Half items (see Tc4Params): one Q tile, slot x reads key tiles [x·nt, x·nt + nt); each step
+// uses two ring entries (slot 0's, then slot 1's) and the epilogue merges the two slots' rows.
 template <bool BF16, int KCH, int BL, int DCH, int EMU, int NSB>
 __global__ void __launch_bounds__(kT4Threads, 1)
     k_chain_tc4(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -282,11 +294,6 @@ __global__ void __launch_bounds__(kT4Threads, 1)
 
   constexpr uint32_t kOCol = NSB * 128;                 // O_0 column; O_1 at kOCol + kOStride
   constexpr uint32_t kOStride = NSB == 3 ? 64 : 128;
-  // The K/V slot of tile g is released by softmax slot kRelX on seeing S of its tile g + kRelD
-  // (slot-tile 2g + 1 + NSB): no tcgen05.commit is spent on the ring (each costs ~220 cycles of
-  // the tensor pipe, tools/commit_bench.cu).  Needs stages > kRelD.
-  constexpr int kRelX = (NSB + 1) & 1;
-  constexpr int kRelD = (NSB + 1) >> 1;
   const int S = p.stages;
   const uint32_t kv_stage = p.b_stage_bytes + p.d_stage_bytes;
   uint8_t* sQ = smem;                                      // [q_bufs][2][q_bytes]
@@ -303,7 +310,7 @@ __global__ void __launch_bounds__(kT4Threads, 1)
   uint64_t* p_full = s_full + 3;    // [NSB] softmax wrote P into buffer b (128 arrivals)
   uint64_t* kv_full = p_full + 3;   // [S] K_g and V_g landed (one barrier: G1 of tile g, which
                                     // precedes both G2 of the tile, is the only waiter)
-  uint64_t* kv_empty = kv_full + S; // [S] both G2 of the tile completed (softmax arrival)
+  uint64_t* kv_empty = kv_full + S; // [S] the last G2 reading the entry completed (commit)
 
   const int warp = threadIdx.x >> 5;
 #if MBCI_TRACE
@@ -356,17 +363,18 @@ __global__ void __launch_bounds__(kT4Threads, 1)
     if (warp == 13) {
       // ============================================================ TMA producer
       if (ptx::elect_one()) {
-        int g = 0, ai = 0;
+        int g = 0, ai = 0;   // g: ring entries used so far
         for (int i = blockIdx.x; i < p.items; i += G) {
           T4Item it;
           it.decode(p, i);
           const int beta = it.u / p.l_mp;
-          const int m0 = (it.u - beta * p.l_mp) * 256;
+          const int m0 = (it.u - beta * p.l_mp) * 256 + (it.half > 0 ? 128 : 0);
           const int nt = it.tiles(t4_nlim(p, beta));
           if (nt == 0) continue;
           const int qb = ai % p.q_bufs;
           if (ai >= p.q_bufs) ptx::mbar_wait(&q_empty[qb], ((ai / p.q_bufs) - 1) & 1);
-          const bool two = m0 + 128 < p.M;   // a fully out-of-range second tile is not loaded
+          // a fully out-of-range second tile is not loaded; a half item has one Q tile
+          const bool two = it.half < 0 && m0 + 128 < p.M;
           ptx::mbar_arrive_expect_tx(&q_full[qb], (two ? 2u : 1u) * p.q_bytes);
           for (int x = 0; x < (two ? 2 : 1); ++x) {
             uint8_t* dst = sQ + (qb * 2 + x) * p.q_bytes;
@@ -375,25 +383,28 @@ __global__ void __launch_bounds__(kT4Threads, 1)
               ptx::tma_load_3d(dst + c * 16384, &tmA, &q_full[qb], c * 64, m0 + x * 128, beta);
           }
           ++ai;
-          for (int j = it.t0; j < it.t0 + nt; ++j, ++g) {
-            const int s = g % S;
-            if (g >= S) ptx::mbar_wait(&kv_empty[s], ((g / S) - 1) & 1);
-            uint8_t* kdst = sKV + s * kv_stage;
-            uint8_t* vdst = kdst + p.b_stage_bytes;
-            if (tr && g < kT4TrTiles) tr[460 + g] = t4_clk();   // K/V load of tile g issued
-            ptx::mbar_arrive_expect_tx(&kv_full[s], p.b_stage_bytes + p.d_stage_bytes);
-            if constexpr (BL == 1) {
+          for (int j = 0; j < nt; ++j) {
+            for (int x = 0; x < (it.half >= 0 ? 2 : 1); ++x, ++g) {
+              const int tile = j + x * nt;   // half item: slot 1 takes tiles [nt, 2 nt)
+              const int s = g % S;
+              if (g >= S) ptx::mbar_wait(&kv_empty[s], ((g / S) - 1) & 1);
+              uint8_t* kdst = sKV + s * kv_stage;
+              uint8_t* vdst = kdst + p.b_stage_bytes;
+              if (tr && g < kT4TrTiles) tr[460 + g] = t4_clk();   // K/V load of entry g issued
+              ptx::mbar_arrive_expect_tx(&kv_full[s], p.b_stage_bytes + p.d_stage_bytes);
+              if constexpr (BL == 1) {
 #pragma unroll
-              for (int c = 0; c < KCH; ++c)
-                ptx::tma_load_3d(kdst + c * (kT4BN * 128), &tmB, &kv_full[s], c * 64, j * kT4BN, beta);
-            } else {
+                for (int c = 0; c < KCH; ++c)
+                  ptx::tma_load_3d(kdst + c * (kT4BN * 128), &tmB, &kv_full[s], c * 64, tile * kT4BN, beta);
+              } else {
 #pragma unroll
-              for (int c = 0; c < kT4BN / 64; ++c)
-                ptx::tma_load_3d(kdst + c * (p.kp_rows * 128), &tmB, &kv_full[s], j * kT4BN + c * 64, 0, beta);
+                for (int c = 0; c < kT4BN / 64; ++c)
+                  ptx::tma_load_3d(kdst + c * (p.kp_rows * 128), &tmB, &kv_full[s], tile * kT4BN + c * 64, 0, beta);
+              }
+#pragma unroll
+              for (int c = 0; c < DCH; ++c)
+                ptx::tma_load_3d(vdst + c * (kT4BN * 128), &tmD, &kv_full[s], c * 64, tile * kT4BN, beta);
             }
-#pragma unroll
-            for (int c = 0; c < DCH; ++c)
-              ptx::tma_load_3d(vdst + c * (kT4BN * 128), &tmD, &kv_full[s], c * 64, j * kT4BN, beta);
           }
         }
       }
@@ -409,7 +420,8 @@ __global__ void __launch_bounds__(kT4Threads, 1)
         T4Cursor c1, c2;   // c1: tile of the next G1, c2: tile of the next G2
         c1.init(p, G);
         c2 = c1;
-        int b1 = 0, b2 = 0, pph = 0;   // S buffer of the next G1 / G2, p_full parity of b2
+        int b1 = 0, b2 = 0;            // S buffer of the next G1 / G2
+        uint32_t pph = 0;              // p_full parity of b2
         int x1 = 0;                    // slot of the next G1
         bool tail_committed = false;
         uint32_t dbg_ph = 0;
@@ -426,12 +438,21 @@ __global__ void __launch_bounds__(kT4Threads, 1)
             if (tr && c1.g < kT4TrTiles) tr[T4TR(c1.g, 12)] = t4_clk();
             if (c1.j == 0) ptx::mbar_spin(&q_full[c1.qb], c1.qph);
             if (!kv_ready) ptx::mbar_spin(&kv_full[c1.st], c1.sph);
+            if (c1.hf) {   // half item: slot 1's K/V is the next ring entry
+              int s1;
+              uint32_t ph1;
+              c1.entry(1, S, s1, ph1);
+              ptx::mbar_spin(&kv_full[s1], ph1);
+            }
             if (tr && c1.g < kT4TrTiles) tr[T4TR(c1.g, 13)] = t4_clk();
             ptx::tc_fence_after();
           }
             const uint64_t tg1 = t4_clk();
-          const uint32_t q_lo = (sQ0 + (c1.qb * 2 + x1) * p.q_bytes) >> 4;
-          const uint32_t k_lo = (sKV0 + c1.st * kv_stage) >> 4;
+          int kst;
+          uint32_t kph;
+          c1.entry(x1, S, kst, kph);
+          const uint32_t q_lo = (sQ0 + (c1.qb * 2 + (c1.hf ? 0 : x1)) * p.q_bytes) >> 4;   // half: one Q tile
+          const uint32_t k_lo = (sKV0 + kst * kv_stage) >> 4;
           const uint32_t dS = tmem + b1 * 128;
 #pragma unroll
           for (int ks = 0; ks < 4 * KCH; ++ks) {
@@ -472,7 +493,10 @@ __global__ void __launch_bounds__(kT4Threads, 1)
           ptx::tc_fence_after();
           const bool kv_ready = c1.valid && x1 == 0 && c1.j != 0 ? ptx::mbar_test(&kv_full[c1.st], c1.sph) : false;
           // G2: O_x2 (+)= P_b2 · V_(c2 tile)
-          const uint32_t v_lo = (sKV0 + c2.st * kv_stage + p.b_stage_bytes) >> 4;
+          int vst;
+          uint32_t vph;
+          c2.entry(x2, S, vst, vph);
+          const uint32_t v_lo = (sKV0 + vst * kv_stage + p.b_stage_bytes) >> 4;
           const uint32_t tO = tmem + kOCol + x2 * kOStride;
           const uint32_t tP = tmem + b2 * 128;
           const uint32_t acc0 = c2.j > 0 ? 1u : 0u;
@@ -487,6 +511,10 @@ __global__ void __launch_bounds__(kT4Threads, 1)
             if (tr && c2.g < kT4TrTiles) tr[T4TR(c2.g, 14 + x2)] = t4_clk() - tg2;
           }
           if (tr && c2.g < kT4TrTiles) tr[T4TR(c2.g, 8 + x2)] = t4_clk();
+          // K/V ring entries are released by a commit after their last reader: G2_1 of a
+          // step, or each G2 of a half item's step (two entries).  (Releasing from the softmax
+          // side two steps later saves this commit but deadlocks when a half item follows.)
+          if (c2.hf || x2 == 1) ptx::mma_commit(&kv_empty[vst]);
           if (c2.j == c2.nt - 1) ptx::mma_commit(&o_full[x2]);
           if (++b2 == NSB) { b2 = 0; pph ^= 1; }
           if (x2 == 1) c2.advance(p, G);
@@ -502,7 +530,6 @@ __global__ void __launch_bounds__(kT4Threads, 1)
     const int row = threadIdx.x - 256;   // TMEM lane (warp 8+w reads lanes 32w..32w+31)
     const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
     using T16 = uint16_t;
-    __shared__ int last_flag;
     int ai = 0;
     auto store_row = [&](T16* erow, int gm, int c0, const float* v, float inv) {
       uint32_t w[8];
@@ -526,128 +553,80 @@ __global__ void __launch_bounds__(kT4Threads, 1)
       const int beta = it.u / p.l_mp;
       const int m0 = (it.u - beta * p.l_mp) * 256;
       const int nt = it.tiles(t4_nlim(p, beta));
+      if (it.half >= 0) {
+        // half item: both slots hold partial (O, m, l) of the same 128 rows (keys split between
+        // them); merge by log-sum-exp, exact in real arithmetic (online-softmax identity)
+        const int gm = m0 + it.half * 128 + row;
+        T16* erow = reinterpret_cast<T16*>(p.E) + static_cast<int64_t>(beta) * p.bs_e +
+                    static_cast<int64_t>(gm) * p.ld_e;
+        float l[2], m[2];
+#pragma unroll
+        for (int x = 0; x < 2; ++x) {
+          ptx::mbar_wait(&o_full[x], ai & 1);
+          ptx::mbar_wait(&l_full[x], ai & 1);
+          l[x] = l_sm[x][ai & 1][row];
+          m[x] = m_sm[x][ai & 1][row];
+          ptx::mbar_arrive(&l_free[x]);
+        }
+        ptx::tc_fence_after();
+        const float mstar = fmaxf(l[0] > 0.f ? m[0] : -INFINITY, l[1] > 0.f ? m[1] : -INFINITY);
+        const float w0 = l[0] > 0.f ? ptx::ex2(m[0] - mstar) : 0.f;
+        const float w1 = l[1] > 0.f ? ptx::ex2(m[1] - mstar) : 0.f;
+        const float L = l[0] * w0 + l[1] * w1;
+        const float inv = L > 0.f ? 1.0f / L : 0.f;
+        const uint32_t tO0 = tmem + lane_off + kOCol, tO1 = tO0 + kOStride;
+#pragma unroll 1
+        for (int c0 = 0; c0 < p.TL; c0 += 16) {
+          uint32_t r0[16], r1[16];
+          ptx::tmem_ld16(tO0 + c0, r0);
+          ptx::tmem_ld16(tO1 + c0, r1);
+          ptx::tmem_wait_ld();
+          float v[16];
+#pragma unroll
+          for (int q = 0; q < 16; ++q) v[q] = w0 * __uint_as_float(r0[q]) + w1 * __uint_as_float(r1[q]);
+          store_row(erow, gm, c0, v, inv);
+        }
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&o_free[0]);
+        ptx::mbar_arrive(&o_free[1]);
+        ++ai;
+        continue;
+      }
 #pragma unroll 1
       for (int x = 0; x < 2; ++x) {
         const int gm = m0 + x * 128 + row;
         T16* erow = reinterpret_cast<T16*>(p.E) + static_cast<int64_t>(beta) * p.bs_e +
                     static_cast<int64_t>(gm) * p.ld_e;
         const uint32_t tO = tmem + lane_off + kOCol + x * kOStride;
-        float l = 0.f, m = -INFINITY;
+        float l = 0.f;
         if (nt > 0) {
           ptx::mbar_wait(&o_full[x], ai & 1);
           ptx::tc_fence_after();
           if (tr && x == 0 && row == 0 && ai < 4) tr[490 + 4 * ai] = t4_clk();
           ptx::mbar_wait(&l_full[x], ai & 1);
           l = l_sm[x][ai & 1][row];
-          m = m_sm[x][ai & 1][row];
           ptx::mbar_arrive(&l_free[x]);
         }
-        if (it.piece < 0) {
-          // whole unit: E = O / l
-          const float inv = l > 0.f ? 1.0f / l : 0.f;
+        // whole unit: E = O / l
+        const float inv = l > 0.f ? 1.0f / l : 0.f;
 #pragma unroll 1
-          for (int c0 = 0; c0 < p.TL; c0 += 16) {
-            float v[16];
-            if (nt > 0) {
-              uint32_t r[16];
-              ptx::tmem_ld16(tO + c0, r);
-              ptx::tmem_wait_ld();
-#pragma unroll
-              for (int q = 0; q < 16; ++q) v[q] = __uint_as_float(r[q]);
-            } else {
-#pragma unroll
-              for (int q = 0; q < 16; ++q) v[q] = 0.f;
-            }
-            store_row(erow, gm, c0, v, inv);
-          }
+        for (int c0 = 0; c0 < p.TL; c0 += 16) {
+          float v[16];
           if (nt > 0) {
-            ptx::tc_fence_before();
-            ptx::mbar_arrive(&o_free[x]);
+            uint32_t r[16];
+            ptx::tmem_ld16(tO + c0, r);
+            ptx::tmem_wait_ld();
+#pragma unroll
+            for (int q = 0; q < 16; ++q) v[q] = __uint_as_float(r[q]);
+          } else {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) v[q] = 0.f;
           }
-        } else {
-          // piece of a tail unit: publish (O, m, l), the last of the unit's pieces merges
-          const int tu = it.u - p.tail;
-          const int64_t prow = (static_cast<int64_t>(tu) * p.pieces + it.piece) * 256 + x * 128 + row;
-          const int64_t n_part = static_cast<int64_t>(p.units - p.tail) * p.pieces * 256;
-          float* wsO = p.ws;
-          float* wsM = p.ws + n_part * p.TL;
-          float* wsL = wsM + n_part;
-          if (nt > 0) {
-#pragma unroll 1
-            for (int c0 = 0; c0 < p.TL; c0 += 16) {
-              uint32_t r[16];
-              ptx::tmem_ld16(tO + c0, r);
-              ptx::tmem_wait_ld();
-              float4* dst = reinterpret_cast<float4*>(wsO + prow * p.TL + c0);
-#pragma unroll
-              for (int q = 0; q < 4; ++q)
-                dst[q] = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
-                                     __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
-            }
-            ptx::tc_fence_before();
-            ptx::mbar_arrive(&o_free[x]);
-          }
-          wsM[prow] = m;
-          wsL[prow] = nt > 0 ? l : 0.f;
-          // release: the barrier orders this warpgroup's stores before thread 0's fence (PTX
-          // fences are cumulative), whose atomic then publishes them at GPU scope
-          ptx::named_bar_sync(1, 128);
-          if (row == 0) {
-            __threadfence();
-            const bool last = atomicAdd(&p.cnt[tu * 2 + x], 1) == p.pieces - 1;
-            if (last) __threadfence();   // acquire the other pieces' partials
-            last_flag = last;
-          }
-          ptx::named_bar_sync(1, 128);
-          if (last_flag) {
-            const int64_t prow0 = static_cast<int64_t>(tu) * p.pieces * 256 + x * 128 + row;
-            float mq[kT4MaxPieces], wq[kT4MaxPieces];
-            float mstar = -INFINITY;
-#pragma unroll
-            for (int q = 0; q < kT4MaxPieces; ++q) {
-              mq[q] = -INFINITY;
-              wq[q] = 0.f;
-              if (q < p.pieces) {
-                wq[q] = __ldcg(wsL + prow0 + q * 256);
-                mq[q] = __ldcg(wsM + prow0 + q * 256);
-              }
-            }
-#pragma unroll
-            for (int q = 0; q < kT4MaxPieces; ++q)
-              if (wq[q] > 0.f) mstar = fmaxf(mstar, mq[q]);
-            float L = 0.f;
-#pragma unroll
-            for (int q = 0; q < kT4MaxPieces; ++q) {
-              const float sc_q = wq[q] > 0.f ? ptx::ex2(mq[q] - mstar) : 0.f;
-              L += wq[q] * sc_q;
-              wq[q] = sc_q;   // now the weight of piece q's O
-            }
-            const float inv = L > 0.f ? 1.0f / L : 0.f;
-#pragma unroll 1
-            for (int c0 = 0; c0 < p.TL; c0 += 16) {
-              float v[16];
-#pragma unroll
-              for (int q = 0; q < 16; ++q) v[q] = 0.f;
-#pragma unroll
-              for (int q = 0; q < kT4MaxPieces; ++q) {
-                if (wq[q] > 0.f) {
-                  const float4* src = reinterpret_cast<const float4*>(wsO + (prow0 + q * 256) * p.TL + c0);
-                  float4 o[4];
-#pragma unroll
-                  for (int c = 0; c < 4; ++c) o[c] = __ldcg(src + c);
-#pragma unroll
-                  for (int c = 0; c < 4; ++c) {
-                    v[4 * c] += wq[q] * o[c].x;
-                    v[4 * c + 1] += wq[q] * o[c].y;
-                    v[4 * c + 2] += wq[q] * o[c].z;
-                    v[4 * c + 3] += wq[q] * o[c].w;
-                  }
-                }
-              }
-              store_row(erow, gm, c0, v, inv);
-            }
-            if (row == 0) p.cnt[tu * 2 + x] = 0;   // ready for the next launch
-          }
+          store_row(erow, gm, c0, v, inv);
+        }
+        if (nt > 0) {
+          ptx::tc_fence_before();
+          ptx::mbar_arrive(&o_free[x]);
         }
         if (tr && row == 0 && ai < 4) tr[490 + 4 * ai + 1 + x] = t4_clk();
       }
@@ -666,9 +645,10 @@ __global__ void __launch_bounds__(kT4Threads, 1)
       T4Item it;
       it.decode(p, i);
       const int beta = it.u / p.l_mp;
-      const int n_lim = t4_nlim(p, beta) - it.t0 * kT4BN;   // keys from this item's first tile on
-      const int nt = it.tiles(n_lim + it.t0 * kT4BN);
+      const int nt = it.tiles(t4_nlim(p, beta));
       if (nt == 0) continue;
+      // keys from this slot's first tile on (a half item's slot 1 starts at tile nt)
+      const int n_lim = t4_nlim(p, beta) - (it.half >= 0 ? x * nt * kT4BN : 0);
       float m_run = 0.f;
       float2 l2 = make_float2(0.f, 0.f), l2b = make_float2(0.f, 0.f);
       for (int j = 0; j < nt; ++j, ++g) {
@@ -677,9 +657,6 @@ __global__ void __launch_bounds__(kT4Threads, 1)
         ptx::mbar_wait(&s_full[b], (k / NSB) & 1);
         ptx::tc_fence_after();
         if (tr && row == 0 && g < kT4TrTiles) tr[T4TR(g, x)] = t4_clk();
-        // S(k) landed => G2(k - NSB) and everything before it completed: the K/V ring slot of
-        // tile g - kRelD (whose last reader is G2(2(g - kRelD) + 1) = G2(k - NSB)) is free.
-        if (x == kRelX && row == 0 && g >= kRelD) ptx::mbar_arrive(&kv_empty[(g - kRelD) % S]);
         if (p.dbg & 1) {
           ptx::tc_fence_before();
           ptx::mbar_arrive(&p_full[b]);

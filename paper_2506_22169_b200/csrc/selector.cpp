@@ -178,7 +178,10 @@ static void score_b200(const mbci_chain_desc_t& d, const mbci_hw_t& hw, mbci_pla
     const int64_t units = b == 0 ? 0 : static_cast<int64_t>(b) * cdiv(d.M, 256);
     const int64_t ntm = std::max<int64_t>(1, nt);
     const int64_t rounds = units / hw.n_sm, rem = units % hw.n_sm;
-    const int64_t tail_tiles = rem > 0 ? ntm : 0;   // the key-axis split of the tail is opt-in
+    // a last round of <= n_sm / 2 units runs as half items (keys split over the two slots)
+    const bool halves = rem > 0 && 2 * rem <= hw.n_sm && ntm % 2 == 0 && d.mask == MBCI_MASK_NONE &&
+                        p.stages >= (p.TL <= 64 ? 4 : 3);
+    const int64_t tail_tiles = rem > 0 ? (halves ? ntm / 2 : ntm) : 0;
     // Calibrated on B200 (round-1 traces, tools/trace_chain4.py): one 256 x 128 score tile of a
     // pair unit costs ~0.75 us + 6 ns per unit of (K + L) (d = 64: 1.5 us, d = 128: 2.3 us) on an
     // SM, plus ~3 us of prologue / epilogue per launch.
@@ -186,7 +189,8 @@ static void score_b200(const mbci_chain_desc_t& d, const mbci_hw_t& hw, mbci_pla
     const double t_pair = (d.op == MBCI_OP_SOFTMAX ? 0.75e-6 + 6.0e-9 * static_cast<double>(p.TK + p.TL)
                                                    : 0.15e-6 + 4.0e-9 * static_cast<double>(p.TK + p.TL)) *
                           (1.965e9 / hw.clock_hz);
-    p.t_b200 = std::max(t_hbm, static_cast<double>(rounds * ntm + tail_tiles) * t_pair) + 3.0e-6;
+    // (ties go to the deeper ring, up to the 4 stages that keep two Q buffers at d = 64)
+    p.t_b200 = std::max(t_hbm, static_cast<double>(rounds * ntm + tail_tiles) * t_pair) + 3.0e-6 - 1e-12 * std::min<int32_t>(p.stages, 4);
     return;
   }
   if (p.kernel == 2 || p.kernel == 3) {

@@ -137,22 +137,22 @@ def test_k4_wide_head_two_stages(mbci, emu):
     check4(mbci, inp, 1.0 / math.sqrt(128), stages=2, rows=rows)
 
 
-@pytest.mark.parametrize("batch,M,N", [(156, 512, 512), (96, 512, 512), (150, 256, 1024), (300, 300, 700)])
-def test_k4_split_tail(mbci, emu, batch, M, N, monkeypatch):
-    """Units beyond the last full round of 148 CTAs are cut along the key axis into pieces whose
-    partial (O, m, l) the last-finishing piece merges (log-sum-exp).  Key padding (incl. 0 and
-    lengths that leave whole pieces empty) and a second launch (merge counters reset) included."""
-    monkeypatch.setenv("MBCI_T4_SPLIT", "1")
-    inp = gen.make_chain_inputs(31 + batch, "f16", batch, M, N, 64, 64, 1, valid_len_range=(0, N))
-    vl = inp.valid_len.copy()
-    vl[-8:] = [0, 1, 127, 128, 129, N, N - 1, 2]
+@pytest.mark.parametrize("batch,M,N", [(156, 512, 512), (96, 512, 512), (150, 256, 1024), (300, 300, 700),
+                                     (4, 200, 250)])
+@pytest.mark.parametrize("halves", ["on", "off"])
+def test_k4_half_items(mbci, emu, batch, M, N, halves, monkeypatch):
+    """A last round of <= 74 pair units runs as half items: one 128-row Q tile per CTA whose two
+    slots split the key tiles, merged by log-sum-exp in the epilogue.  Sampled rows plus every
+    row of the last pair units (the half items), both settings, and run-to-run determinism."""
+    if halves == "off":
+        monkeypatch.setenv("MBCI_T4_NO_HALF", "1")
+    inp = gen.make_chain_inputs(31 + batch, "f16", batch, M, N, 64, 64, 1, sigmas=(2.0, 2.0, 1.0))
+    last = batch - 1
     rows = np.stack([np.arange(batch), (np.arange(batch) * 101) % M], axis=1).astype(np.int64)
-    rows = np.concatenate([rows, np.array([[batch - 1, M - 1], [batch - 2, 0], [batch - 5, M // 2]])])
-    E1, ch = check4(mbci, inp, 0.125, valid_len=vl, rows=rows)
-    E2, _ = run_chain(mbci, inp, "softmax", 0.125, vl, plan=k4_plan(mbci, 64))
+    rows = np.concatenate([rows, np.stack([np.full(M, last), np.arange(M)], axis=1)]).astype(np.int64)
+    E1, ch = check4(mbci, inp, 0.125, rows=rows, stages=4)   # halves need a 4-deep ring at d = 64
+    E2, _ = run_chain(mbci, inp, "softmax", 0.125, plan=k4_plan(mbci, 64, stages=4))
     assert torch.equal(E1.view(torch.int16), E2.view(torch.int16))
-    got = e_f64(E1, "f16")
-    assert np.all(got[-8] == 0.0)
 
 
 def test_k4_deterministic(mbci, emu):
