@@ -569,11 +569,14 @@ __global__ void __launch_bounds__(kT4Threads, 1)
           ptx::mbar_arrive(&l_free[x]);
         }
         ptx::tc_fence_after();
-        const float mstar = fmaxf(l[0] > 0.f ? m[0] : -INFINITY, l[1] > 0.f ? m[1] : -INFINITY);
-        const float w0 = l[0] > 0.f ? ptx::ex2(m[0] - mstar) : 0.f;
-        const float w1 = l[1] > 0.f ? ptx::ex2(m[1] - mstar) : 0.f;
-        const float L = l[0] * w0 + l[1] * w1;
-        const float inv = L > 0.f ? 1.0f / L : 0.f;
+        float w0 = 1.f, w1 = 1.f, inv = 1.f;   // NONE / SCALE: E = O_0 + O_1
+        if (p.op == 2) {
+          const float mstar = fmaxf(l[0] > 0.f ? m[0] : -INFINITY, l[1] > 0.f ? m[1] : -INFINITY);
+          w0 = l[0] > 0.f ? ptx::ex2(m[0] - mstar) : 0.f;
+          w1 = l[1] > 0.f ? ptx::ex2(m[1] - mstar) : 0.f;
+          const float L = l[0] * w0 + l[1] * w1;
+          inv = L > 0.f ? 1.0f / L : 0.f;
+        }
         const uint32_t tO0 = tmem + lane_off + kOCol, tO1 = tO0 + kOStride;
 #pragma unroll 1
         for (int c0 = 0; c0 < p.TL; c0 += 16) {

@@ -214,6 +214,20 @@ def test_k4_plain_chain_ragged(mbci, M, N, K, L):
         assert err <= BUDGET["bf16"], (op, err, ch.describe())
 
 
+@pytest.mark.parametrize("op", ["none", "scale"])
+def test_k4_plain_chain_half_items(mbci, op):
+    """NONE / SCALE through half items: the two slots' partial products are summed (no
+    normalisation).  156 x 512 rows -> 312 pair units -> the last 16 run as half items."""
+    b, M, N, K = 156, 512, 512, 64
+    inp = gen.make_chain_inputs(5, "bf16", b, M, N, K, K, 1, sigmas=(1.0, 1.0 / math.sqrt(K), 1.0 / math.sqrt(N)))
+    E, ch = run_chain(mbci, inp, op, 0.5 if op == "scale" else 1.0, plan=k4_plan(mbci, K, stages=4))
+    rows = np.concatenate([np.stack([np.full(M, b - 1), np.arange(M)], axis=1),
+                           np.stack([np.arange(b), (np.arange(b) * 37) % M], axis=1)]).astype(np.int64)
+    ref = oracle.chain(inp, op, 0.5 if op == "scale" else 1.0, rows=rows)
+    err = oracle.row_max_error(e_f64(E, "bf16")[rows[:, 0], rows[:, 1]], ref)
+    assert err <= BUDGET["bf16"], (err, ch.describe())
+
+
 def test_k4_plain_chain_C4_shape_sampled(mbci):
     b, M, N, K = 64, 2048, 2048, 64
     inp = gen.make_chain_inputs(0, "bf16", b, M, N, K, K, 0, sigmas=(1.0, 1.0 / math.sqrt(K), 1.0 / math.sqrt(N)))
