@@ -164,3 +164,32 @@ def test_rule3_fallback_keeps_a_plan_on_ragged_N(m):
     st, plans = m.plan_enumerate(m.make_desc(2, 200, 300, 64, 64, "bf16"))
     assert st == m.MBCI_OK and plans
     assert all(model.rule3_reject(300, p.BN) for p in plans)
+
+
+def test_kernel4_plans_for_attention_shapes(m):
+    """Kernel 4 (persistent ping-pong) is the default for 16-bit chains of every op; its plans use
+    the whole L per CTA, 128-key tiles, fit SMEM with room for the static (l, m) arrays, and the
+    4-stage plan (which enables half items for the last partial round) ranks first on C2."""
+    hw = m.hw_default()
+    for op in ("softmax", "scale", "none"):
+        d = m.make_desc(96, 512, 512, 64, 64, "f16", op, 0.125)
+        st, plans = m.plan_enumerate(d, hw)
+        assert st == m.MBCI_OK and plans[0].kernel == 4
+    d = m.make_desc(96, 512, 512, 64, 64, "f16", "softmax", 0.125)
+    st, plans = m.plan_enumerate(d, hw)
+    k4 = [p for p in plans if p.kernel == 4]
+    assert k4[0].stages == 4 and all(p.stages >= 3 for p in k4)
+    by_stages = {p.stages: p.t_b200 for p in k4}
+    assert by_stages[4] < by_stages[3]          # half items (stages >= 4) halve the tail round
+    for p in k4:
+        assert p.BN == 128 and p.TL == 64 and p.BM == 256 and p.tmem_cols == 512
+        assert p.smem_bytes + 5120 <= hw.smem_max
+    # key padding disables half items: the 3- and 4-stage plans then score alike
+    d = m.make_desc(96, 512, 512, 64, 64, "f16", "softmax", 0.125, mask=True)
+    st, plans = m.plan_enumerate(d, hw)
+    k4 = {p.stages: p.t_b200 for p in plans if p.kernel == 4}
+    assert abs(k4[4] - k4[3]) < 1e-9
+    # d = 128 (C5 shape): two S buffers, a 2-deep ring is the only fit with the Q pair
+    d = m.make_desc(512, 4096, 4096, 128, 128, "bf16", "softmax", 0.125)
+    st, plans = m.plan_enumerate(d, hw)
+    assert plans[0].kernel == 4 and plans[0].stages == 2 and plans[0].TL == 128
