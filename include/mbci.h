@@ -82,7 +82,12 @@ typedef struct {
 
 /* One candidate plan: the paper's tile sizes (T_M, T_N, T_K, T_H) for the
  * flat expression mh(n(k(L_A,L_B,C_C),L_D,C_E),S_E), plus B200 pipeline parameters and the
- * model terms of Eqs. (2)-(5).  kernel: 0 = tcgen05 fused chain, 1 = SIMT (CUDA cores). */
+ * model terms of Eqs. (2)-(5).  kernel: 4 = persistent ping-pong tcgen05 chain (default for
+ * 16-bit inputs: pairs of 128-row Q tiles per CTA, BM = 256, BN = 128, TL = L padded to 16,
+ * stages >= 3 when L <= 64; stages >= 4 enables half items for the last partial round),
+ * 0 = one tcgen05 CTA per (β, 128-row tile, h-chunk), 2 / 3 = persistent stream-K variants,
+ * 1 = SIMT (CUDA cores; fp32 and TMA-illegal strides).  n_block: CTAs (kernel 0/1) or work
+ * items (kernels 2-4) of the created plan. */
 typedef struct {
   int32_t kernel;
   int32_t BM, BN, TK, TL;   /* T_M, T_N, T_K (= padded K: dead k loop), T_H */
