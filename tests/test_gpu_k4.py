@@ -155,6 +155,16 @@ def test_k4_half_items(mbci, emu, batch, M, N, halves, monkeypatch):
     assert torch.equal(E1.view(torch.int16), E2.view(torch.int16))
 
 
+@pytest.mark.parametrize("dtype,b_layout,K,L", [("bf16", 0, 64, 64), ("bf16", 1, 48, 40), ("f16", 0, 32, 64)])
+def test_k4_half_items_layouts(mbci, dtype, b_layout, K, L):
+    """Half items with B stored [K, N] (MN-major K tiles), bf16, and head dims below 64."""
+    batch, M, N = 150, 256, 512
+    inp = gen.make_chain_inputs(77 + K, dtype, batch, M, N, K, L, b_layout)
+    rows = np.concatenate([np.stack([np.full(M, batch - 1), np.arange(M)], axis=1),
+                           np.stack([np.arange(batch), (np.arange(batch) * 53) % M], axis=1)]).astype(np.int64)
+    check4(mbci, inp, 1.0 / math.sqrt(K), rows=rows, stages=4)
+
+
 def test_k4_deterministic(mbci, emu):
     inp = gen.make_chain_inputs(17, "f16", 16, 512, 512, 64, 64, 1)
     E1, _ = run_chain(mbci, inp, "softmax", 0.125, plan=k4_plan(mbci, 64))
