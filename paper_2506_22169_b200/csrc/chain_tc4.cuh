@@ -22,10 +22,15 @@
 //   of the S buffer it came from.  tcgen05 ops of one thread complete in issue order, so a G1
 //   rewrites a buffer only after the G2 that read its P.
 // * Exponentials: z = s·log2(e)·S − m with packed f32x2 FMA; p = 2^z on the MUFU (ex2.approx)
-//   or, for EMU of every 8 column pairs (default 2, MBCI_T4_EMU), on the FMA pipe (Cody–Waite split + degree-3 minimax
-//   polynomial, max rel. error 8.8e-5 < the 16-bit P rounding) so both pipes share the work.
+//   or, for EMU of every 8 column pairs (default 2, MBCI_T4_EMU), on the FMA pipe (Cody–Waite
+//   split + degree-3 minimax polynomial, max rel. error 8.8e-5 < the 16-bit P rounding), so
+//   both pipes share the work.
 //   Lazy rescale: the running max only moves when a tile's max exceeds it by > τ = 8 (log2),
 //   exact in real arithmetic (R4).
+//
+// * Wave quantisation: a last, partial round of <= n_SM / 2 units runs as "half" items (one
+//   128-row Q tile, the two slots split its key tiles, the epilogue merges them by log-sum-exp),
+//   so that round costs half the tiles (Tc4Params).
 //
 // Warps: 0-3 softmax slot 0 | 4-7 softmax slot 1 | 8-11 epilogue | 12 tcgen05 issuer + TMEM
 //        allocator | 13 TMA producer | 14-15 idle.  setmaxnreg moves registers to the softmax
