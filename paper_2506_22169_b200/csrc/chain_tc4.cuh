@@ -323,14 +323,45 @@ __global__ void __launch_bounds__(kT4Threads, 1)
 #else
   constexpr uint64_t* tr = nullptr;
 #endif
-  if (threadIdx.x == 0) {
-    if (tr) {
-      tr[0] = ptx::globaltimer();
-      tr[4] = t4_clk();
-      uint32_t smid;
-      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-      tr[2] = smid;
+  if (tr && threadIdx.x == 0) {
+    tr[0] = ptx::globaltimer();
+    tr[4] = t4_clk();
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    tr[2] = smid;
+  }
+  // The TMA warp initialises the barriers and issues the first item's Q and first K/V ring
+  // entries before the CTA-wide barrier, so their HBM latency overlaps TMEM allocation and the
+  // set-up of the other roles (all other threads touch the barriers only after __syncthreads).
+  int pre_entries = 0;   // TMA warp: entries of the first active item already issued
+  auto load_entry = [&](int s, int tile, int beta) {
+    uint8_t* kdst = sKV + s * kv_stage;
+    uint8_t* vdst = kdst + p.b_stage_bytes;
+    ptx::mbar_arrive_expect_tx(&kv_full[s], p.b_stage_bytes + p.d_stage_bytes);
+    if constexpr (BL == 1) {
+#pragma unroll
+      for (int c = 0; c < KCH; ++c)
+        ptx::tma_load_3d(kdst + c * (kT4BN * 128), &tmB, &kv_full[s], c * 64, tile * kT4BN, beta);
+    } else {
+#pragma unroll
+      for (int c = 0; c < kT4BN / 64; ++c)
+        ptx::tma_load_3d(kdst + c * (p.kp_rows * 128), &tmB, &kv_full[s], tile * kT4BN + c * 64, 0, beta);
     }
+#pragma unroll
+    for (int c = 0; c < DCH; ++c)
+      ptx::tma_load_3d(vdst + c * (kT4BN * 128), &tmD, &kv_full[s], c * 64, tile * kT4BN, beta);
+  };
+  // Q of an item into Q buffer qb (two tiles, or one for a half item / a pair past M)
+  auto load_q = [&](int qb, int m0, int beta, bool two) {
+    ptx::mbar_arrive_expect_tx(&q_full[qb], (two ? 2u : 1u) * p.q_bytes);
+    for (int x = 0; x < (two ? 2 : 1); ++x) {
+      uint8_t* dst = sQ + (qb * 2 + x) * p.q_bytes;
+#pragma unroll
+      for (int c = 0; c < KCH; ++c)
+        ptx::tma_load_3d(dst + c * 16384, &tmA, &q_full[qb], c * 64, m0 + x * 128, beta);
+    }
+  };
+  if (warp == 13 && ptx::elect_one()) {
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&q_full[i], 1);
       ptx::mbar_init(&q_empty[i], 1);
@@ -349,11 +380,24 @@ __global__ void __launch_bounds__(kT4Threads, 1)
       ptx::mbar_init(&kv_empty[s], 1);
     }
     ptx::fence_mbar_init();
-  }
-  if (warp == 13) {
     ptx::tma_prefetch(&tmA);
     ptx::tma_prefetch(&tmB);
     ptx::tma_prefetch(&tmD);
+    if (!(p.dbg & 32)) {
+      for (int i = blockIdx.x; i < p.items; i += gridDim.x) {
+        T4Item it;
+        it.decode(p, i);
+        const int beta = it.u / p.l_mp;
+        const int m0 = (it.u - beta * p.l_mp) * 256 + (it.half > 0 ? 128 : 0);
+        const int nt = it.tiles(t4_nlim(p, beta));
+        if (nt == 0) continue;
+        load_q(0, m0, beta, it.half < 0 && m0 + 128 < p.M);
+        const int per = it.half >= 0 ? 2 : 1;
+        pre_entries = min(S, nt * per);
+        for (int e = 0; e < pre_entries; ++e) load_entry(e, e / per + (e % per) * nt, beta);
+        break;
+      }
+    }
   }
   if (warp == 12) ptx::tmem_alloc(&tmem_base_slot, 512);
   ptx::tc_fence_before();
@@ -378,37 +422,18 @@ __global__ void __launch_bounds__(kT4Threads, 1)
           if (nt == 0) continue;
           const int qb = ai % p.q_bufs;
           if (ai >= p.q_bufs) ptx::mbar_wait(&q_empty[qb], ((ai / p.q_bufs) - 1) & 1);
-          // a fully out-of-range second tile is not loaded; a half item has one Q tile
-          const bool two = it.half < 0 && m0 + 128 < p.M;
-          ptx::mbar_arrive_expect_tx(&q_full[qb], (two ? 2u : 1u) * p.q_bytes);
-          for (int x = 0; x < (two ? 2 : 1); ++x) {
-            uint8_t* dst = sQ + (qb * 2 + x) * p.q_bytes;
-#pragma unroll
-            for (int c = 0; c < KCH; ++c)
-              ptx::tma_load_3d(dst + c * 16384, &tmA, &q_full[qb], c * 64, m0 + x * 128, beta);
-          }
+          // a fully out-of-range second tile is not loaded; a half item has one Q tile; the
+          // first item's Q (and its first entries) went out before the CTA barrier
+          if (ai > 0 || pre_entries == 0) load_q(qb, m0, beta, it.half < 0 && m0 + 128 < p.M);
           ++ai;
           for (int j = 0; j < nt; ++j) {
             for (int x = 0; x < (it.half >= 0 ? 2 : 1); ++x, ++g) {
+              if (g < pre_entries) continue;
               const int tile = j + x * nt;   // half item: slot 1 takes tiles [nt, 2 nt)
               const int s = g % S;
               if (g >= S) ptx::mbar_wait(&kv_empty[s], ((g / S) - 1) & 1);
-              uint8_t* kdst = sKV + s * kv_stage;
-              uint8_t* vdst = kdst + p.b_stage_bytes;
               if (tr && g < kT4TrTiles) tr[460 + g] = t4_clk();   // K/V load of entry g issued
-              ptx::mbar_arrive_expect_tx(&kv_full[s], p.b_stage_bytes + p.d_stage_bytes);
-              if constexpr (BL == 1) {
-#pragma unroll
-                for (int c = 0; c < KCH; ++c)
-                  ptx::tma_load_3d(kdst + c * (kT4BN * 128), &tmB, &kv_full[s], c * 64, tile * kT4BN, beta);
-              } else {
-#pragma unroll
-                for (int c = 0; c < kT4BN / 64; ++c)
-                  ptx::tma_load_3d(kdst + c * (p.kp_rows * 128), &tmB, &kv_full[s], tile * kT4BN + c * 64, 0, beta);
-              }
-#pragma unroll
-              for (int c = 0; c < DCH; ++c)
-                ptx::tma_load_3d(vdst + c * (kT4BN * 128), &tmD, &kv_full[s], c * 64, tile * kT4BN, beta);
+              load_entry(s, tile, beta);
             }
           }
         }
