@@ -8,9 +8,12 @@ A "step" is one fused-chain launch over the whole batch (every §8(a) row on the
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl {cuda,reference}]
                     [--config C2|C3|C4-16|...|C6] [--no-cpu-baseline]
 
-Multi-GPU (torchrun, one rank per GPU): weak scaling — every rank runs the full
-per-GPU batch of the config on its own shard of β; no collective on the
-data path; NCCL only for the barrier and the MAX over ranks of device time.
+Multi-GPU (one rank per GPU; `--gpus N` re-launches itself under torch.distributed.run when
+WORLD_SIZE is unset): rank r owns the contiguous β range [r·b/g, (r+1)·b/g) of the global batch
+(SURVEY §8(e)).  `--scaling strong` (default for C2 and C5) splits the config's batch over the
+ranks; `--scaling weak` gives every rank the full per-GPU batch.  No collective on the data
+path; NCCL only for the barrier, the MAX over ranks of device time, the SUM of bytes and,
+after timing, an all-gather of E that the cpu_baseline leg checks against the oracle on rank 0.
 
 Timing: inputs resident in HBM; `rot` sets of (A, B, D, E) used round-robin so the
 working set between reuses exceeds 2x L2 (126 MB) — no step hits L2-resident inputs;
@@ -163,6 +166,31 @@ def time_oracle(name, min_seconds, max_slices=None, seed=0):
     return gbs, sample, cores, sec_per
 
 
+def gather_check(name, seed, E_all, slices, rows_per_slice=32):
+    """cpu_baseline leg, rank 0: sampled rows of the gathered E (every rank's shard) against the
+    oracle, each slice's inputs regenerated from the seeded generator (batch_start = β)."""
+    import numpy as np
+    import mbci_inputs as gen
+    import oracle
+    dtype, b, M, N, K, L, op, desc, s, bytes_, flops, exps = cfg_numbers(name)
+    sc = 1.0 / math.sqrt(K) if op == "softmax" else 1.0
+    sig = (1.0, 1.0, 1.0) if op == "softmax" else (1.0, 1.0 / math.sqrt(K), 1.0 / math.sqrt(N))
+    rng = np.random.default_rng(seed + 17)
+    worst = 0.0
+    nrows = 0
+    for beta in slices:
+        inp = gen.make_chain_inputs(seed, dtype, 1, M, N, K, L, 1 if op == "softmax" else 0, sigmas=sig,
+                                    batch_start=int(beta))
+        ms = np.unique(np.concatenate([[0, M - 1], rng.integers(0, M, rows_per_slice - 2)])).astype(np.int64)
+        rows = np.stack([np.zeros_like(ms), ms], axis=1)
+        ref = oracle.chain(inp, op, sc, rows=rows)
+        got = gen.bits_to_f64_numpy(np.ascontiguousarray(E_all[int(beta)][ms]), dtype)
+        worst = max(worst, oracle.row_max_error(got, ref))
+        nrows += len(ms)
+    tol = 1e-5 if dtype == "f32" else 2e-2
+    return {"slices": [int(x) for x in slices], "rows": nrows, "max_row_err": worst, "tol": tol, "ok": worst <= tol}
+
+
 def run_reference(args, rank, world):
     """--impl reference: the CPU oracle as it stands, on rank 0 only."""
     if rank != 0:
@@ -188,7 +216,7 @@ def run_reference(args, rank, world):
     line = {
         "impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": desc, "name": name, "batch_heads": b, "M": M, "N": N, "K": K, "L": L, "op": op,
                    "sample_batch_heads_per_step": nsl, "parallelism": "host cores (OpenMP)"},
         "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "oracle", "sample": sample},
@@ -215,8 +243,11 @@ def run_cuda(args, rank, world, local_rank):
     sc = 1.0 / math.sqrt(K) if op == "softmax" else 1.0
     sig = (1.0, 1.0, 1.0) if op == "softmax" else (1.0, 1.0 / math.sqrt(K), 1.0 / math.sqrt(N))
 
-    # this rank's shard of a weak-scaling global batch of b * world
-    lo, hi = sharding.shard_range(b * world, rank, world)
+    # this rank's shard: strong scaling splits the config's batch, weak scaling keeps b per rank
+    global_b = b if args.scaling == "strong" else b * world
+    lo, hi = sharding.shard_range(global_b, rank, world)
+    counts = [sharding.shard_range(global_b, r, world)[1] - sharding.shard_range(global_b, r, world)[0]
+              for r in range(world)]
     nb = hi - lo
     inp = gen.make_chain_inputs(args.seed, dtype, nb, M, N, K, L, b_layout, sigmas=sig, batch_start=lo)
 
@@ -311,6 +342,15 @@ def run_cuda(args, rank, world, local_rank):
     d2h = pE.numel() * s
     e2e_gbs = total_bytes / (e2e_ms * 1e-3) / 1e9
 
+    # ---- after timing: gather E of every shard to rank 0 (NCCL), checked in the cpu_baseline leg
+    A0, B0, D0, E0 = sets[0]
+    with torch.cuda.stream(stream):
+        ch.run_ptr(A0.data_ptr(), B0.data_ptr(), D0.data_ptr(), E0.data_ptr(), 0, stream.cuda_stream)
+    stream.synchronize()
+    E_bits = E0.view(torch.int32 if dtype == "f32" else torch.int16)
+    E_all = sharding.gather_shards(E_bits, counts) if world > 1 else E_bits
+    E_all = E_all.cpu().numpy().view(np.uint32 if dtype == "f32" else np.uint16) if rank == 0 else None
+
     if rank != 0:
         return
     pk = peaks()
@@ -319,10 +359,17 @@ def run_cuda(args, rank, world, local_rank):
     traffic = _traffic(name, world)
     roofline = {"bound": "hbm", "achieved": gbs / world, "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": frac, "traffic": traffic, "peak_src": pk["src"],
-                "kernel": {0: "k_chain_tc", 1: "k_chain_simt", 2: "k_chain_tc2", 3: "k_chain_tc3", 4: "k_chain_tc4"}.get(plan.kernel, "?"),
+                "kernel": {0: "k_chain_tc", 1: "k_chain_simt", 4: "k_chain_tc4", 5: "k_chain_tc5"}.get(plan.kernel, "?"),
                 "per_launch_bytes": step_bytes, "per_launch_us": ms_per_step * 1e3,
                 "tensor_tflops": tflops / world, "tensor_frac": tflops / world / pk["bf16_tflops"],
                 "ex2_per_s": (exps * nb / b) / (ms_per_step * 1e-3) if exps else 0.0}
+    gcheck = None
+    if not args.no_cpu_baseline:
+        # one slice from each end of every rank's shard, at most 16 in all
+        sl = sorted({x for r in range(world) for x in (sharding.shard_range(global_b, r, world)[0],
+                                                         sharding.shard_range(global_b, r, world)[1] - 1)})
+        sl = sl[:: max(1, len(sl) // 16)][:16]
+        gcheck = gather_check(name, args.seed, E_all, sl)
     if not args.no_cpu_baseline and world == 1:
         cgbs, sample, cores, _ = time_oracle(name, args.cpu_seconds)
         cpu = {"value": cgbs, "unit": "GB/s", "cores": cores, "kind": "oracle", "sample": sample}
@@ -331,13 +378,13 @@ def run_cuda(args, rank, world, local_rank):
     line = {
         "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "us_per_chain": ms_per_step * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dtype, "data": "synthetic",
-        "config": {"workload": desc, "name": name, "batch_heads_per_gpu": b, "global_batch_heads": b * world,
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": dtype, "data": "synthetic",
+        "config": {"workload": desc, "name": name, "batch_heads_per_gpu": nb, "global_batch_heads": global_b,
                    "M": M, "N": N, "K": K, "L": L, "op": op, "scale": sc, "b_layout": b_layout,
                    "l2": f"{rot} rotating input sets ({rot * step_bytes / 2**20:.0f} MiB) > 2x L2 between reuses",
                    "timing": "K steps in one CUDA graph, CUDA events on the launch stream, max over ranks",
                    "parallelism": f"dp{world} (batch x head sharding, no data-path collective)",
-                   "plan": ch.describe()},
+                   "plan": ch.describe(), "env": {k: v for k, v in os.environ.items() if k.startswith("MBCI_")}},
         "hbm_frac_of_8TBps": gbs / (8000.0 * world),
         "roofline": roofline,
         "cpu_baseline": cpu,
@@ -345,6 +392,7 @@ def run_cuda(args, rank, world, local_rank):
                 "d2h_bytes_per_step": d2h, "api": "mbci_chain_run_host"},
         "gpu_launches": launches * args.steps,
         "clocks": clocks,
+        "gather_check": gcheck,
     }
     print(json.dumps(line), flush=True)
     ch.close()
@@ -373,6 +421,27 @@ def _traffic(name, world):
         return None
 
 
+def _free_port() -> int:
+    import socket
+    so = socket.socket()
+    so.bind(("127.0.0.1", 0))
+    port = so.getsockname()[1]
+    so.close()
+    return port
+
+
+def relaunch_cmd(argv, n_gpus, port):
+    """`bench.py --gpus N` without WORLD_SIZE: the torch.distributed.run command that starts one
+    rank per GPU on this node (rendezvous on 127.0.0.1)."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n_gpus}",
+            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + list(argv)
+
+
+def default_scaling(config: str) -> str:
+    """C2 and C5 split the global batch over the ranks (strong scaling)."""
+    return "strong" if config in ("C2", "C5") else "weak"
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -380,20 +449,29 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["cuda", "reference"], default="cuda")
     ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--scaling", choices=["strong", "weak"], default=None,
+                    help="strong: split the config's batch over the ranks; weak: full batch per rank")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--tune", type=int, default=0)
-    ap.add_argument("--plan", default="", help="force a plan BN:TL:stages (tensor-core path)")
+    ap.add_argument("--plan", default="", help="force a plan kernel:BN:TL:stages (tensor-core path)")
     ap.add_argument("--sustain", type=float, default=1.0, help="seconds of untimed load for the clock sampler")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.scaling is None:
+        args.scaling = default_scaling(args.config)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(subprocess.call(relaunch_cmd(sys.argv[1:], args.gpus, _free_port())))
+    if os.environ.get("MBCI_T4_DEBUG") or os.environ.get("MBCI_LIB") == "trace":
+        print(json.dumps({"error": "MBCI_T4_DEBUG / MBCI_LIB=trace are diagnostics builds; bench refuses them"}))
+        sys.exit(2)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    if args.gpus != world and world > 1:
-        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    if args.gpus != world:
+        print(f"[bench] warning: --gpus {args.gpus} but WORLD_SIZE {world}; using {world} rank(s)", file=sys.stderr)
     if args.impl == "reference":
         return run_reference(args, rank, world)
     if world > 1:
@@ -401,6 +479,11 @@ def main():
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        t = torch.ones(1, device="cuda")
+        dist.all_reduce(t)   # creates the NCCL communicator now, not inside the timed region
+        print(f"[bench] rank {rank}/{world} (local {local_rank}, {torch.cuda.get_device_name(local_rank)}): "
+              f"NCCL communicator ready, nranks={int(t.item())}, nccl {'.'.join(map(str, torch.cuda.nccl.version()))}",
+              file=sys.stderr, flush=True)
     try:
         run_cuda(args, rank, world, local_rank)
     finally:

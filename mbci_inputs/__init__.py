@@ -20,6 +20,9 @@ that every dtype holds exactly.
 """
 from __future__ import annotations
 
+import os
+from concurrent.futures import ThreadPoolExecutor
+
 import numpy as np
 
 __all__ = [
@@ -69,13 +72,22 @@ def normal_bits(seed: int, tensor: str, start: int, count: int, dtype: str,
                 sigma: float = 1.0, chunk: int = 1 << 24) -> np.ndarray:
     """``count`` N(0, sigma^2) draws (elements start..start+count-1 of tensor) as raw storage bits."""
     out = np.empty(count, dtype=np.uint32 if dtype == "f32" else np.uint16)
-    for c0 in range(0, count, chunk):
+
+    def fill(c0):
         n = min(chunk, count - c0)
         x = _counters(seed, tensor, start + c0, n)
         u1 = ((x >> np.uint64(32)).astype(np.float64) + 0.5) * (1.0 / 4294967296.0)
         u2 = ((x & np.uint64(0xFFFFFFFF)).astype(np.float64) + 0.5) * (1.0 / 4294967296.0)
         z = np.sqrt(-2.0 * np.log(u1)) * np.cos(2.0 * np.pi * u2)
         out[c0:c0 + n] = _f64_to_storage(sigma * z, dtype)
+
+    starts = range(0, count, chunk)
+    if len(starts) > 1:   # disjoint chunks; numpy releases the GIL, so host threads help at C5 sizes
+        with ThreadPoolExecutor(max_workers=min(len(starts), os.cpu_count() or 1, 32)) as ex:
+            list(ex.map(fill, starts))
+    else:
+        for c0 in starts:
+            fill(c0)
     return out
 
 

@@ -17,9 +17,8 @@
 #include "../../include/mbci.h"
 #include "chain_simt.cuh"
 #include "chain_tc.cuh"
-#include "chain_tc2.cuh"
-#include "chain_tc3.cuh"
 #include "chain_tc4.cuh"
+#include "chain_tc5.cuh"
 #include "selector.h"
 
 using namespace mbci;
@@ -107,46 +106,6 @@ TcKernel pick_tc(bool bf16, int bn, int kch, int bl, int dch) {
   return bf16 ? pick_bn<true>(bn, kch, bl, dch) : pick_bn<false>(bn, kch, bl, dch);
 }
 
-using Tc2Kernel = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, Tc2Params);
-
-template <bool BF16, int BN, int KCH, int BL>
-Tc2Kernel pick2_d(int dch) {
-  return dch == 1 ? (Tc2Kernel)k_chain_tc2<BF16, BN, KCH, BL, 1> : (Tc2Kernel)k_chain_tc2<BF16, BN, KCH, BL, 2>;
-}
-template <bool BF16, int BN, int KCH>
-Tc2Kernel pick2_bl(int bl, int dch) {
-  return bl == 0 ? pick2_d<BF16, BN, KCH, 0>(dch) : pick2_d<BF16, BN, KCH, 1>(dch);
-}
-template <bool BF16, int BN>
-Tc2Kernel pick2_kch(int kch, int bl, int dch) {
-  return kch == 1 ? pick2_bl<BF16, BN, 1>(bl, dch) : pick2_bl<BF16, BN, 2>(bl, dch);
-}
-template <bool BF16>
-Tc2Kernel pick2_bn(int bn, int kch, int bl, int dch) {
-  // the two-slot kernel keeps S double-buffered + O in 256 TMEM columns per slot: BN = 64 only
-  return bn == 64 ? pick2_kch<BF16, 64>(kch, bl, dch) : nullptr;
-}
-Tc2Kernel pick_tc2(bool bf16, int bn, int kch, int bl, int dch) {
-  return bf16 ? pick2_bn<true>(bn, kch, bl, dch) : pick2_bn<false>(bn, kch, bl, dch);
-}
-
-using Tc3Kernel = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, Tc3Params);
-template <bool BF16, int KCH, int BL>
-Tc3Kernel pick3_d(int dch) {
-  return dch == 1 ? (Tc3Kernel)k_chain_tc3<BF16, KCH, BL, 1> : (Tc3Kernel)k_chain_tc3<BF16, KCH, BL, 2>;
-}
-template <bool BF16, int KCH>
-Tc3Kernel pick3_bl(int bl, int dch) {
-  return bl == 0 ? pick3_d<BF16, KCH, 0>(dch) : pick3_d<BF16, KCH, 1>(dch);
-}
-template <bool BF16>
-Tc3Kernel pick3_kch(int kch, int bl, int dch) {
-  return kch == 1 ? pick3_bl<BF16, 1>(bl, dch) : pick3_bl<BF16, 2>(bl, dch);
-}
-Tc3Kernel pick_tc3(bool bf16, int kch, int bl, int dch) {
-  return bf16 ? pick3_kch<true>(kch, bl, dch) : pick3_kch<false>(kch, bl, dch);
-}
-
 using Tc4Kernel = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, Tc4Params);
 template <bool BF16, int KCH, int BL, int DCH>
 Tc4Kernel pick4_emu(int emu) {
@@ -170,11 +129,44 @@ Tc4Kernel pick_tc4(bool bf16, int kch, int bl, int dch, int emu) {
   return kch == 1 ? pick4_bl<false, 1>(bl, dch, emu) : pick4_bl<false, 2>(bl, dch, emu);
 }
 
+using Tc5Kernel = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, Tc4Params);
+template <bool BF16, int KCH, int BL>
+Tc5Kernel pick5_emu(int emu) {
+  switch (emu) {
+    case 0: return (Tc5Kernel)k_chain_tc5<BF16, KCH, BL, 0>;
+    case 2: return (Tc5Kernel)k_chain_tc5<BF16, KCH, BL, 2>;
+    case 4: return (Tc5Kernel)k_chain_tc5<BF16, KCH, BL, 4>;
+    default: return (Tc5Kernel)k_chain_tc5<BF16, KCH, BL, 3>;
+  }
+}
+template <bool BF16, int KCH>
+Tc5Kernel pick5_bl(int bl, int emu) {
+  return bl == 0 ? pick5_emu<BF16, KCH, 0>(emu) : pick5_emu<BF16, KCH, 1>(emu);
+}
+Tc5Kernel pick_tc5(bool bf16, int kch, int bl, int emu) {
+  if (bf16) return kch == 1 ? pick5_bl<true, 1>(bl, emu) : pick5_bl<true, 2>(bl, emu);
+  return kch == 1 ? pick5_bl<false, 1>(bl, emu) : pick5_bl<false, 2>(bl, emu);
+}
+
+// Kernel-5 feature flags (Tc4Params::flags); MBCI_T5_FLAGS overrides (diagnostics).
+int t5_flags_default() {
+  const char* e = getenv("MBCI_T5_FLAGS");
+  if (e) return atoi(e) & 0x3F;
+  return 17;  // bit 0: exp-phase turns; bit 2: spinning single-thread waits (A/B only);
+              // bits 4-5: hand the turn over that many 16-pair chunks before the end
+}
+
+// Programmatic dependent launch for kernel 5 (MBCI_PDL=0 disables it, for A/B measurements).
+bool pdl_enabled() {
+  const char* e = getenv("MBCI_PDL");
+  return !(e && e[0] == '0');
+}
+
 // Pairs of every 8 exponential pairs evaluated by the FMA-pipe polynomial in kernel 4
 // (MBCI_T4_EMU overrides; 0 = all on the MUFU).
 int t4_emu_default() {
   const char* e = getenv("MBCI_T4_EMU");
-  if (e && (e[0] == '0' || e[0] == '2' || e[0] == '3')) return e[0] - '0';
+  if (e && (e[0] == '0' || e[0] == '2' || e[0] == '3' || e[0] == '4')) return e[0] - '0';
   return 2;   // 2/8 of the pairs: C2 21.0 us, C3 61.7 (3/8: 21.5, 63.1; 0: 22.2, 65.4; 4/8 slower)
 }
 
@@ -214,8 +206,8 @@ mbci_status_t encode3d(CUtensorMap* map, const void* base, bool bf16, int64_t co
 }
 
 struct MapCacheEntry {
-  const void *A = nullptr, *B = nullptr, *D = nullptr;
-  CUtensorMap ta, tb, td;
+  const void *A = nullptr, *B = nullptr, *D = nullptr, *E = nullptr;
+  CUtensorMap ta, tb, td, te;
   uint64_t stamp = 0;
 };
 
@@ -228,17 +220,12 @@ struct mbci_chain {
   // tensor-core path
   TcKernel tc = nullptr;
   TcParams tp{};
-  Tc2Kernel tc2 = nullptr;
-  Tc2Params tp2{};
-  Tc3Kernel tc3 = nullptr;
-  Tc3Params tp3{};
-  Tc4Kernel tc4 = nullptr;
+  Tc4Kernel tc4 = nullptr;   // kernel 4
+  Tc5Kernel tc5 = nullptr;   // kernel 5 (same parameter block, plus E's tensor map)
   Tc4Params tp4{};
   int32_t grid2 = 0;
-  void* ws2 = nullptr;     // stream-K partials + flags (kernel 2)
-  size_t ws2_bytes = 0;
   int32_t kch = 1, dch = 1;
-  MapCacheEntry cache[8];
+  MapCacheEntry cache[16];   // tensor maps of the 16 most recent (A, B, D) pointer triples
   uint64_t stamp = 0;
   uint64_t* trace = nullptr;
   // end-to-end scratch
@@ -287,84 +274,28 @@ mbci_status_t setup_plan(mbci_chain* h) {
     t.idesc1 = ptx::idesc_f16(fmt, 0, d.b_layout == 0 ? 1u : 0u, 128, (uint32_t)p.BN);
     t.idesc2 = ptx::idesc_f16(fmt, 0, 1u, 128, (uint32_t)p.TL);
     p.n_block = (int64_t)d.batch * t.l_m * t.l_h;
+    if (p.n_block > INT32_MAX) return fail(MBCI_ERR_UNSUPPORTED, "kernel-0 grid exceeds 2^31 - 1 CTAs");
     cudaError_t e = cudaFuncSetAttribute((const void*)h->tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          p.smem_bytes);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
-  } else if (p.kernel == 2) {
-    const int32_t k_steps = static_cast<int32_t>((d.K + 15) / 16);
-    Tc2Layout lay;
-    if (!tc2_layout(k_steps, p.BN, p.TL, p.stages, d.b_layout, &lay))
-      return fail(MBCI_ERR_UNSUPPORTED, "kernel-2 plan does not fit SMEM/TMEM");
-    p.smem_bytes = lay.smem_total;
-    p.tmem_cols = 512;
-    h->kch = std::max(1, (16 * k_steps + 63) / 64);
-    h->dch = (p.TL + 63) / 64;
-    h->tc2 = pick_tc2(d.dtype == MBCI_BF16, p.BN, h->kch, d.b_layout, h->dch);
-    if (!h->tc2) return fail(MBCI_ERR_UNSUPPORTED, "kernel-2 plan needs BN = 64");
-    Tc2Params& t = h->tp2;
-    t = Tc2Params{};
-    t.M = (int32_t)d.M; t.N = (int32_t)d.N; t.K = (int32_t)d.K; t.L = (int32_t)d.L;
-    t.batch = (int32_t)d.batch;
-    t.l_m = (int32_t)((d.M + 127) / 128);
-    t.l_h = (int32_t)((d.L + p.TL - 1) / p.TL);
-    t.TL = p.TL;
-    t.k_steps = k_steps;
-    t.stages = p.stages;
-    t.a_bufs = lay.a_bufs;
-    t.op = d.op;
-    t.scale = d.op == MBCI_OP_SOFTMAX ? d.scale * 1.4426950408889634f : d.scale;
-    t.ld_e = d.ld_e;
-    t.bs_e = d.bs_e;
-    t.a_bytes = (uint32_t)lay.a_bytes;
-    t.b_stage_bytes = (uint32_t)lay.b_stage;
-    t.d_stage_bytes = (uint32_t)lay.d_stage;
-    t.kp_rows = (uint32_t)(16 * k_steps);
-    t.slot_bytes = (uint32_t)lay.slot_bytes;
-    const uint32_t fmt = d.dtype == MBCI_BF16 ? 1u : 0u;
-    t.idesc1 = ptx::idesc_f16(fmt, 0, d.b_layout == 0 ? 1u : 0u, 128, (uint32_t)p.BN);
-    t.idesc2 = ptx::idesc_f16(fmt, 0, 1u, 128, (uint32_t)p.TL);
-    t.tpu = (int32_t)std::max<int64_t>(1, (d.N + p.BN - 1) / p.BN);
-    const int64_t units = (int64_t)d.batch * t.l_m * t.l_h;
-    if (units * t.tpu > INT32_MAX) return fail(MBCI_ERR_UNSUPPORTED, "kernel-2 tile count exceeds int32");
-    t.W = (int32_t)(units * t.tpu);
-    int n_sm = 148;
-    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, h->device);
-    const char* one = getenv("MBCI_DEBUG_ONE_SLOT");
-    t.slots_per_cta = (one && one[0] == '1') ? 1 : 2;
-    h->grid2 = (int32_t)std::max<int64_t>(1, std::min<int64_t>(n_sm, (t.W + t.slots_per_cta - 1) / t.slots_per_cta));
-    t.n_slots = t.slots_per_cta * h->grid2;
-    p.n_block = units;
-    cudaError_t e = cudaFuncSetAttribute((const void*)h->tc2, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         p.smem_bytes);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
-    int occ = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)h->tc2, kT2Threads, p.smem_bytes);
-    if (e != cudaSuccess) return cuda_fail(e, "occupancy query");
-    if (occ < 1) return fail(MBCI_ERR_UNSUPPORTED, "kernel-2 CTA does not fit on an SM");
-    // workspace: partial O [P][128][TL] fp32 + (m, l) [P][2][128] + flags [P]
-    const size_t ws_floats = (size_t)t.n_slots * 128 * p.TL + (size_t)t.n_slots * 256;
-    const size_t need = ws_floats * 4 + (size_t)t.n_slots * 4;
-    if (h->ws2_bytes < need) {
-      if (h->ws2) cudaFree(h->ws2);
-      h->ws2 = nullptr;
-      h->ws2_bytes = 0;
-      if (cudaMalloc(&h->ws2, need) != cudaSuccess) return fail(MBCI_ERR_NOMEM, "stream-K workspace");
-      h->ws2_bytes = need;
-    }
-    e = cudaMemset(h->ws2, 0, need);
-    if (e != cudaSuccess) return cuda_fail(e, "workspace memset");
-    t.ws = static_cast<float*>(h->ws2);
-    t.flags = reinterpret_cast<int32_t*>(static_cast<float*>(h->ws2) + ws_floats);
-  } else if (p.kernel == 4) {
+  } else if (p.kernel == 4 || p.kernel == 5) {
     const int32_t k_steps = static_cast<int32_t>((d.K + 15) / 16);
     Tc4Layout lay;
-    if (k_steps < 1 || d.N < 1 || !tc4_layout(k_steps, p.TL, p.stages, d.b_layout, &lay))
-      return fail(MBCI_ERR_UNSUPPORTED, "kernel-4 plan needs K, N >= 1 and must fit SMEM/TMEM");
+    const bool fits = p.kernel == 5 ? tc5_layout(k_steps, p.TL, p.stages, d.b_layout, &lay)
+                                    : tc4_layout(k_steps, p.TL, p.stages, d.b_layout, &lay);
+    if (k_steps < 1 || d.N < 1 || !fits)
+      return fail(MBCI_ERR_UNSUPPORTED, "kernel-%d plan needs K, N >= 1 and must fit SMEM/TMEM", p.kernel);
     p.smem_bytes = lay.smem_total;
     p.tmem_cols = 512;
     h->kch = std::max(1, (16 * k_steps + 63) / 64);
     h->dch = (p.TL + 63) / 64;
-    h->tc4 = pick_tc4(d.dtype == MBCI_BF16, h->kch, d.b_layout, h->dch, t4_emu_default());
+    h->tc4 = nullptr;
+    h->tc5 = nullptr;
+    if (p.kernel == 5)
+      h->tc5 = pick_tc5(d.dtype == MBCI_BF16, h->kch, d.b_layout, t4_emu_default());
+    else
+      h->tc4 = pick_tc4(d.dtype == MBCI_BF16, h->kch, d.b_layout, h->dch, t4_emu_default());
+    const void* kfn = p.kernel == 5 ? (const void*)h->tc5 : (const void*)h->tc4;
     Tc4Params& t = h->tp4;
     t = Tc4Params{};
     t.M = (int32_t)d.M; t.N = (int32_t)d.N; t.K = (int32_t)d.K; t.L = (int32_t)d.L;
@@ -381,7 +312,10 @@ mbci_status_t setup_plan(mbci_chain* h) {
     t.scale = d.op == MBCI_OP_SOFTMAX ? d.scale * 1.4426950408889634f : (d.op == MBCI_OP_SCALE ? d.scale : 1.0f);
     t.ld_e = d.ld_e;
     t.bs_e = d.bs_e;
+#if MBCI_TRACE
+    // work-skipping diagnostics exist only in the trace build (libmbci_trace.so)
     if (const char* dbg = getenv("MBCI_T4_DEBUG")) t.dbg = atoi(dbg);
+#endif
     t.q_bytes = (uint32_t)lay.q_bytes;
     t.b_stage_bytes = (uint32_t)lay.b_stage;
     t.d_stage_bytes = (uint32_t)lay.d_stage;
@@ -405,74 +339,16 @@ mbci_status_t setup_plan(mbci_chain* h) {
     t.items = (int32_t)(halves ? t.half_from + 2 * rem : units);
     h->grid2 = (int32_t)std::max<int64_t>(1, std::min<int64_t>(n_sm, t.items));
     p.n_block = t.items;
-    cudaError_t e = cudaFuncSetAttribute((const void*)h->tc4, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         p.smem_bytes);
+    t.flags = p.kernel == 5 ? t5_flags_default() : 0;
+    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_bytes);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
     int occ = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)h->tc4, kT4Threads, p.smem_bytes);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, p.kernel == 5 ? kT5Threads : kT4Threads,
+                                                      p.smem_bytes);
     if (e != cudaSuccess) return cuda_fail(e, "occupancy query");
-    if (occ < 1) return fail(MBCI_ERR_UNSUPPORTED, "kernel-4 CTA does not fit on an SM");
-  } else if (p.kernel == 3) {
-    const int32_t k_steps = static_cast<int32_t>((d.K + 15) / 16);
-    Tc3Layout lay;
-    if (!tc3_layout(k_steps, p.TL, p.stages, d.b_layout, &lay))
-      return fail(MBCI_ERR_UNSUPPORTED, "kernel-3 plan does not fit SMEM/TMEM");
-    p.smem_bytes = lay.smem_total;
-    p.tmem_cols = 512;
-    h->kch = std::max(1, (16 * k_steps + 63) / 64);
-    h->dch = (p.TL + 63) / 64;
-    h->tc3 = pick_tc3(d.dtype == MBCI_BF16, h->kch, d.b_layout, h->dch);
-    Tc3Params& t = h->tp3;
-    t = Tc3Params{};
-    t.M = (int32_t)d.M; t.N = (int32_t)d.N; t.K = (int32_t)d.K; t.L = (int32_t)d.L;
-    t.batch = (int32_t)d.batch;
-    t.l_mp = (int32_t)((d.M + 255) / 256);
-    t.l_h = (int32_t)((d.L + p.TL - 1) / p.TL);
-    t.TL = p.TL;
-    t.k_steps = k_steps;
-    t.stages = p.stages;
-    t.q_bufs = lay.q_bufs;
-    t.op = d.op;
-    t.scale = d.op == MBCI_OP_SOFTMAX ? d.scale * 1.4426950408889634f : d.scale;
-    t.ld_e = d.ld_e;
-    t.bs_e = d.bs_e;
-    t.q_bytes = (uint32_t)lay.q_bytes;
-    t.b_stage_bytes = (uint32_t)lay.b_stage;
-    t.d_stage_bytes = (uint32_t)lay.d_stage;
-    t.kp_rows = (uint32_t)(16 * k_steps);
-    const uint32_t fmt = d.dtype == MBCI_BF16 ? 1u : 0u;
-    t.idesc1 = ptx::idesc_f16(fmt, 0, d.b_layout == 0 ? 1u : 0u, 128, 128u);
-    t.idesc2 = ptx::idesc_f16(fmt, 0, 1u, 128, (uint32_t)p.TL);
-    t.tpu = (int32_t)std::max<int64_t>(1, (d.N + 127) / 128);
-    const int64_t units = (int64_t)d.batch * t.l_mp * t.l_h;
-    if (units * t.tpu > INT32_MAX) return fail(MBCI_ERR_UNSUPPORTED, "kernel-3 tile count exceeds int32");
-    t.W = (int32_t)(units * t.tpu);
-    int n_sm = 148;
-    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, h->device);
-    h->grid2 = (int32_t)std::max<int64_t>(1, std::min<int64_t>(n_sm, t.W));
-    t.n_ctas = h->grid2;
-    p.n_block = units;
-    cudaError_t e = cudaFuncSetAttribute((const void*)h->tc3, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         p.smem_bytes);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
-    int occ = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)h->tc3, kT3Threads, p.smem_bytes);
-    if (e != cudaSuccess) return cuda_fail(e, "occupancy query");
-    if (occ < 1) return fail(MBCI_ERR_UNSUPPORTED, "kernel-3 CTA does not fit on an SM");
-    const size_t ws_floats = (size_t)t.n_ctas * 256 * p.TL + (size_t)t.n_ctas * 512;
-    const size_t need = ws_floats * 4 + (size_t)t.n_ctas * 4;
-    if (h->ws2_bytes < need) {
-      if (h->ws2) cudaFree(h->ws2);
-      h->ws2 = nullptr;
-      h->ws2_bytes = 0;
-      if (cudaMalloc(&h->ws2, need) != cudaSuccess) return fail(MBCI_ERR_NOMEM, "stream-K workspace");
-      h->ws2_bytes = need;
-    }
-    e = cudaMemset(h->ws2, 0, need);
-    if (e != cudaSuccess) return cuda_fail(e, "workspace memset");
-    t.ws = static_cast<float*>(h->ws2);
-    t.flags = reinterpret_cast<int32_t*>(static_cast<float*>(h->ws2) + ws_floats);
+    if (occ < 1) return fail(MBCI_ERR_UNSUPPORTED, "kernel-%d CTA does not fit on an SM", p.kernel);
   } else {
+    if (d.batch * d.M > INT32_MAX) return fail(MBCI_ERR_UNSUPPORTED, "batch * M exceeds the CUDA-core grid");
     p.n_block = d.batch * d.M;
     const void* fn = d.dtype == MBCI_F32 ? (const void*)k_chain_simt<float>
                      : d.dtype == MBCI_F16 ? (const void*)k_chain_simt<__half>
@@ -495,13 +371,13 @@ mbci_status_t launch(mbci_chain* h, const void* A, const void* B, const void* D,
   if (d.mask == MBCI_MASK_KEY_PADDING && !valid_len)
     return fail(MBCI_ERR_INVALID, "mask KEY_PADDING needs valid_len");
   const int32_t* vl = d.mask == MBCI_MASK_KEY_PADDING ? valid_len : nullptr;
-  if (h->plan.kernel == 0 || h->plan.kernel == 2 || h->plan.kernel == 3 || h->plan.kernel == 4) {
+  if (h->plan.kernel == 0 || h->plan.kernel == 4 || h->plan.kernel == 5) {
     if (!aligned16(E) || (d.N > 0 && !aligned16(D)) || (d.K > 0 && d.N > 0 && (!aligned16(A) || !aligned16(B))))
       return fail(MBCI_ERR_UNSUPPORTED, "tensor-core path needs 16-byte aligned A, B, D, E");
     // tensor maps (cached by pointer triple)
     MapCacheEntry* ent = nullptr;
     for (auto& c : h->cache)
-      if (c.stamp && c.A == A && c.B == B && c.D == D) ent = &c;
+      if (c.stamp && c.A == A && c.B == B && c.D == D && c.E == E) ent = &c;
     if (!ent) {
       ent = &h->cache[0];
       for (auto& c : h->cache)
@@ -512,7 +388,8 @@ mbci_status_t launch(mbci_chain* h, const void* A, const void* B, const void* D,
       memset(&ent->ta, 0, sizeof(CUtensorMap));
       memset(&ent->tb, 0, sizeof(CUtensorMap));
       memset(&ent->td, 0, sizeof(CUtensorMap));
-      const uint32_t bn_box = (h->plan.kernel == 3 || h->plan.kernel == 4) ? 128u : (uint32_t)h->plan.BN;
+      memset(&ent->te, 0, sizeof(CUtensorMap));
+      const uint32_t bn_box = (h->plan.kernel == 4 || h->plan.kernel == 5) ? 128u : (uint32_t)h->plan.BN;
       if (d.K > 0 && d.N > 0) {
         s = encode3d(&ent->ta, A, bf16, d.K, d.M, d.batch, d.ld_a, d.bs_a, 128);
         if (s != MBCI_OK) return s;
@@ -527,9 +404,14 @@ mbci_status_t launch(mbci_chain* h, const void* A, const void* B, const void* D,
         s = encode3d(&ent->td, D, bf16, d.L, d.N, d.batch, d.ld_d, d.bs_d, bn_box);
         if (s != MBCI_OK) return s;
       }
+      if (h->plan.kernel == 5) {   // E: TMA bulk stores of 128-row x 64-column tiles
+        s = encode3d(&ent->te, E, bf16, d.L, d.M, d.batch, d.ld_e, d.bs_e, 128);
+        if (s != MBCI_OK) return s;
+      }
       ent->A = A;
       ent->B = B;
       ent->D = D;
+      ent->E = E;
     }
     ent->stamp = ++h->stamp;
     if (h->plan.kernel == 0) {
@@ -544,40 +426,23 @@ mbci_status_t launch(mbci_chain* h, const void* A, const void* B, const void* D,
       t.E = E;
       t.trace = h->trace;
       h->tc4<<<(unsigned)h->grid2, kT4Threads, h->plan.smem_bytes, st>>>(ent->ta, ent->tb, ent->td, t);
-    } else if (h->plan.kernel == 3) {
-      Tc3Params t = h->tp3;
-      t.valid_len = vl;
-      t.E = E;
-      t.trace = h->trace;
-      cudaLaunchConfig_t cfg{};
-      cfg.gridDim = dim3((unsigned)h->grid2);
-      cfg.blockDim = dim3(kT3Threads);
-      cfg.dynamicSmemBytes = (size_t)h->plan.smem_bytes;
-      cfg.stream = st;
-      cudaLaunchAttribute attr[1];
-      attr[0].id = cudaLaunchAttributeCooperative;   // co-residency: stream-K finishers wait on peers
-      attr[0].val.cooperative = 1;
-      cfg.attrs = attr;
-      cfg.numAttrs = 1;
-      cudaError_t le = cudaLaunchKernelEx(&cfg, h->tc3, ent->ta, ent->tb, ent->td, t);
-      if (le != cudaSuccess) return cuda_fail(le, "cooperative launch");
     } else {
-      Tc2Params t = h->tp2;
+      Tc4Params t = h->tp4;
       t.valid_len = vl;
       t.E = E;
       t.trace = h->trace;
       cudaLaunchConfig_t cfg{};
       cfg.gridDim = dim3((unsigned)h->grid2);
-      cfg.blockDim = dim3(kT2Threads);
+      cfg.blockDim = dim3(kT5Threads);
       cfg.dynamicSmemBytes = (size_t)h->plan.smem_bytes;
       cfg.stream = st;
       cudaLaunchAttribute attr[1];
-      attr[0].id = cudaLaunchAttributeCooperative;   // co-residency: stream-K finishers wait on peers
-      attr[0].val.cooperative = 1;
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // chain_tc5.cuh header
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
       cfg.attrs = attr;
-      cfg.numAttrs = 1;
-      cudaError_t le = cudaLaunchKernelEx(&cfg, h->tc2, ent->ta, ent->tb, ent->td, t);
-      if (le != cudaSuccess) return cuda_fail(le, "cooperative launch");
+      cfg.numAttrs = pdl_enabled() ? 1 : 0;
+      cudaError_t le = cudaLaunchKernelEx(&cfg, h->tc5, ent->ta, ent->tb, ent->td, ent->te, t);
+      if (le != cudaSuccess) return cuda_fail(le, "kernel-5 launch");
     }
   } else {
     SimtParams sp{};
@@ -622,8 +487,21 @@ mbci_status_t check_device(int device) {
   return MBCI_OK;
 }
 
+// Seeded non-zero scratch inputs for tuning (equal scores would hide the rescale work):
+// 16-bit normals via a counter hash + Box-Muller approximation-free mapping to [-2, 2).
+__global__ void k_tune_fill(uint16_t* x, int64_t n, uint32_t seed, int bf16) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t z = (uint64_t)i * 0x9E3779B97F4A7C15ull + seed;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    const float v = (float)((z >> 40) & 0xFFFFFF) * (4.0f / 16777216.0f) - 2.0f;
+    x[i] = bf16 ? __bfloat16_as_ushort(__float2bfloat16(v)) : __half_as_ushort(__float2half(v));
+  }
+}
+
 mbci_status_t tune_plan(mbci_chain* h, const std::vector<mbci_plan_t>& plans) {
-  // PAPER.md Alg. 1 lines 5-9: estimate all, measure the top n = 8.
+  // PAPER.md Alg. 1 lines 5-9: estimate all, measure the top n = 8.  A candidate
+  // whose set-up or launch fails is skipped, never timed.
   const mbci_chain_desc_t& d = h->d;
   const int64_t s = elem_size(d);
   const int64_t b_rows = d.b_layout == 0 ? d.K : d.N, b_cols = d.b_layout == 0 ? d.N : d.K;
@@ -637,7 +515,7 @@ mbci_status_t tune_plan(mbci_chain* h, const std::vector<mbci_plan_t>& plans) {
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   mbci_status_t rc = MBCI_OK;
   float best = 1e30f;
-  mbci_plan_t best_plan = plans[0];
+  int best_i = -1;
   const int n_try = std::min<int>(8, (int)plans.size());
   if (cudaMalloc(&A, std::max<size_t>(nA, 16)) != cudaSuccess || cudaMalloc(&B, std::max<size_t>(nB, 16)) != cudaSuccess ||
       cudaMalloc(&D, std::max<size_t>(nD, 16)) != cudaSuccess || cudaMalloc(&E, std::max<size_t>(nE, 16)) != cudaSuccess ||
@@ -645,38 +523,50 @@ mbci_status_t tune_plan(mbci_chain* h, const std::vector<mbci_plan_t>& plans) {
     rc = fail(MBCI_ERR_NOMEM, "tune scratch allocation failed");
     goto done;
   }
-  cudaMemset(A, 0, nA);
-  cudaMemset(B, 0, nB);
-  cudaMemset(D, 0, nD);
+  cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  if (s == 2) {
+    k_tune_fill<<<256, 256, 0, st>>>((uint16_t*)A, (int64_t)(nA / 2), 1u, d.dtype == MBCI_BF16);
+    k_tune_fill<<<256, 256, 0, st>>>((uint16_t*)B, (int64_t)(nB / 2), 2u, d.dtype == MBCI_BF16);
+    k_tune_fill<<<256, 256, 0, st>>>((uint16_t*)D, (int64_t)(nD / 2), 3u, d.dtype == MBCI_BF16);
+  } else {
+    cudaMemsetAsync(A, 0, nA, st);
+    cudaMemsetAsync(B, 0, nB, st);
+    cudaMemsetAsync(D, 0, nD, st);
+  }
   {
     std::vector<int32_t> hv(std::max<int64_t>(d.batch, 1), (int32_t)d.N);
-    cudaMemcpy(V, hv.data(), hv.size() * 4, cudaMemcpyHostToDevice);
+    cudaMemcpyAsync(V, hv.data(), hv.size() * 4, cudaMemcpyHostToDevice, st);
+    cudaStreamSynchronize(st);
   }
-  cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   for (int i = 0; i < n_try; ++i) {
     h->plan = plans[i];
     for (auto& c : h->cache) c = MapCacheEntry{};
-    rc = setup_plan(h);
-    if (rc != MBCI_OK) goto done;
-    for (int w = 0; w < 2; ++w) launch(h, A, B, D, E, V, st);
+    if (setup_plan(h) != MBCI_OK) continue;
+    bool ok = true;
+    for (int w = 0; w < 2 && ok; ++w) ok = launch(h, A, B, D, E, V, st) == MBCI_OK;
     cudaEventRecord(e0, st);
-    for (int r = 0; r < 5; ++r) launch(h, A, B, D, E, V, st);
+    for (int r = 0; r < 5 && ok; ++r) ok = launch(h, A, B, D, E, V, st) == MBCI_OK;
     cudaEventRecord(e1, st);
     cudaError_t ce = cudaEventSynchronize(e1);
-    if (ce != cudaSuccess) {
+    if (ce != cudaSuccess) {   // a device fault poisons the context: report it
       rc = cuda_fail(ce, "tuning run");
       goto done;
     }
+    if (!ok || cudaGetLastError() != cudaSuccess) continue;
     float ms = 0.f;
     cudaEventElapsedTime(&ms, e0, e1);
     if (ms < best) {
       best = ms;
-      best_plan = plans[i];
+      best_i = i;
     }
   }
-  h->plan = best_plan;
+  if (best_i < 0) {
+    rc = fail(MBCI_ERR_UNSUPPORTED, "tuning: no candidate plan launched successfully");
+    goto done;
+  }
+  h->plan = plans[best_i];
   for (auto& c : h->cache) c = MapCacheEntry{};
   rc = setup_plan(h);
 done:
@@ -691,6 +581,19 @@ done:
   return rc;
 }
 
+// Restores the caller's current device on scope exit (the ABI never leaves it changed).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
 mbci_status_t create_impl(const mbci_chain_desc_t* desc, int device, const mbci_plan_t* forced,
                           mbci_chain_t* out) {
   if (!out) return fail(MBCI_ERR_INVALID, "out is NULL");
@@ -700,8 +603,7 @@ mbci_status_t create_impl(const mbci_chain_desc_t* desc, int device, const mbci_
   if (s != MBCI_OK) return s;
   s = check_device(device);
   if (s != MBCI_OK) return s;
-  cudaError_t e = cudaSetDevice(device);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  DeviceGuard guard(device);
   mbci_hw_t hw;
   hw_default(&hw);
   cudaDeviceProp prop;
@@ -738,7 +640,7 @@ mbci_status_t create_impl(const mbci_chain_desc_t* desc, int device, const mbci_
     // The shortlist keeps the best-ranked plans of every kernel family so that a model error
     // between families cannot hide the fastest kernel.
     std::vector<mbci_plan_t> shortlist;
-    for (int fam : {4, 0, 2, 3, 1}) {
+    for (int fam : {5, 4, 0, 1}) {
       int taken = 0;
       for (const auto& q : plans)
         if (q.kernel == fam && taken < 3) {
@@ -781,6 +683,7 @@ mbci_status_t mbci_chain_create_with_plan(const mbci_chain_desc_t* desc, int dev
 mbci_status_t mbci_chain_run(mbci_chain_t h, const void* A, const void* B, const void* D, void* E,
                              const int32_t* valid_len, void* stream) {
   if (!h) return fail(MBCI_ERR_INVALID, "handle is NULL");
+  DeviceGuard guard(h->device);   // launch on the handle's device, restore the caller's
   return launch(h, A, B, D, E, valid_len, reinterpret_cast<cudaStream_t>(stream));
 }
 
@@ -796,8 +699,8 @@ mbci_status_t mbci_chain_run_host(mbci_chain_t h, const void* A, const void* B, 
   const size_t nB = span_elems(d.batch, b_rows, b_cols, d.ld_b, d.bs_b) * s;
   const size_t nD = span_elems(d.batch, d.N, d.L, d.ld_d, d.bs_d) * s;
   const size_t nE = span_elems(d.batch, d.M, d.L, d.ld_e, d.bs_e) * s;
-  cudaError_t e = cudaSetDevice(h->device);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  DeviceGuard guard(h->device);
+  cudaError_t e = cudaSuccess;
   auto ensure = [&](void** p, size_t* have, size_t need) -> bool {
     if (*have >= need && *p) return true;
     if (*p) cudaFree(*p);
@@ -839,7 +742,6 @@ mbci_status_t mbci_chain_run_host(mbci_chain_t h, const void* A, const void* B, 
 
 mbci_status_t mbci_chain_destroy(mbci_chain_t h) {
   if (!h) return MBCI_OK;
-  cudaFree(h->ws2);
   cudaFree(h->dA);
   cudaFree(h->dB);
   cudaFree(h->dD);
@@ -861,16 +763,14 @@ mbci_status_t mbci_chain_describe(mbci_chain_t h, char* buf, size_t len) {
   snprintf(buf, len,
            "kernel=%s BM=%d BN=%d TK=%d TL=%d stages=%d smem=%d tmem=%d n_block=%lld "
            "t_estm=%.3gs alpha=%.4f t_b200=%.3gs",
-           p.kernel == 0 ? "tcgen05" : (p.kernel == 2 ? "tcgen05-streamk" : (p.kernel == 3 ? "tcgen05-pair-streamk" : (p.kernel == 4 ? "tcgen05-pingpong" : "simt"))), p.BM, p.BN, p.TK, p.TL, p.stages, p.smem_bytes, p.tmem_cols,
+           p.kernel == 0 ? "tcgen05" : (p.kernel == 4 ? "tcgen05-pingpong" : (p.kernel == 5 ? "tcgen05-pingpong-sepP" : "simt")), p.BM, p.BN, p.TK, p.TL, p.stages, p.smem_bytes, p.tmem_cols,
            (long long)p.n_block, p.t_estm, p.alpha, p.t_b200);
   return MBCI_OK;
 }
 
 mbci_status_t mbci_chain_set_trace(mbci_chain_t h, void* buf, int64_t cap_bytes) {
   if (!h) return fail(MBCI_ERR_INVALID, "handle is NULL");
-  const int64_t need = h->plan.kernel == 2   ? (int64_t)h->tp2.n_slots * 256 * 8
-                       : h->plan.kernel == 3 ? (int64_t)h->tp3.n_ctas * 256 * 8
-                       : h->plan.kernel == 4 ? (int64_t)h->grid2 * kT4TraceSlots * 8
+  const int64_t need = (h->plan.kernel == 4 || h->plan.kernel == 5) ? (int64_t)h->grid2 * kT4TraceSlots * 8
                                              : h->plan.n_block * kTraceSlots * 8;
   if (buf && cap_bytes < need) return fail(MBCI_ERR_INVALID, "trace buffer needs %lld bytes", (long long)need);
   h->trace = static_cast<uint64_t*>(buf);

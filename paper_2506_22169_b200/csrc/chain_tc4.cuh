@@ -71,6 +71,8 @@ struct Tc4Params {
   // (O, m, l) rows inside the CTA (log-sum-exp).  Only without key padding and with nt_max even.
   int32_t items, half_from, nt_max;
   uint64_t* trace;         // [gridDim.x][kT4TraceSlots] (MBCI_TRACE builds only)
+  int32_t flags;           // kernel 5: bit 0 = exp-phase turns between the two slots' warps of an
+                           // SMSP, bit 2 = issuer / TMA threads spin on test_wait (A/B only)
   int32_t dbg;             // diagnostics only (MBCI_T4_DEBUG): 1 = softmax skips its TMEM/math work,
                            // 2 = issuer skips the G2 MMAs, 4 = issuer skips the G1 MMAs
 };

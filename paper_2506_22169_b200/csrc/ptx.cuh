@@ -123,6 +123,10 @@ __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+__device__ __forceinline__ void named_bar_arrive(uint32_t id, uint32_t nthreads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
 __device__ __forceinline__ void st_release_gpu(int32_t* addr, int32_t v) {
   asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(addr), "r"(v) : "memory");
 }
@@ -143,6 +147,14 @@ __device__ __forceinline__ void spin_acquire_gpu(const int32_t* addr, int32_t v)
     if (globaltimer() - t0 > 4000000000ull) __trap();
   }
 }
+
+// ---------------------------------------------------------------- programmatic dependent launch
+// griddepcontrol.wait: block until every prerequisite grid (launched before this one in the
+// stream) has completed and its memory is visible; a no-op without a programmatic dependency.
+__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// griddepcontrol.launch_dependents: the next grid of the stream (if launched with programmatic
+// stream serialisation) may be scheduled once every CTA of this grid has issued it or exited.
+__device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // ---------------------------------------------------------------- TMA
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
@@ -173,6 +185,15 @@ __device__ __forceinline__ void tma_store_commit() {
 
 __device__ __forceinline__ void tma_store_wait_all() {
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// The shared-memory source of every committed bulk store has been read (it may be rewritten).
+__device__ __forceinline__ void tma_store_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
 
 __device__ __forceinline__ void fence_proxy_async_smem() {

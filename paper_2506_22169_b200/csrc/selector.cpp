@@ -78,41 +78,6 @@ int64_t tc_smem_bytes(int32_t k_steps, int32_t BN, int32_t TL, int32_t stages, i
          1024;  // + alignment slack for the 1024-B swizzle atoms
 }
 
-bool tc2_layout(int32_t k_steps, int32_t BN, int32_t TL, int32_t stages, int32_t b_layout, Tc2Layout* out,
-                int32_t smem_max) {
-  if (2 * BN + TL > 256) return false;  // per-slot TMEM: S double-buffered (P aliased) + O
-  int32_t a, b, d;
-  tc_smem_bytes(k_steps, BN, TL, stages, b_layout, &a, &b, &d);
-  for (int32_t a_bufs = 2; a_bufs >= 1; --a_bufs) {
-    const int32_t bars = 8 * (4 + 4 * stages + 6);
-    int32_t slot = a_bufs * a + stages * (b + d) + bars;
-    slot = (slot + 1023) & ~1023;
-    const int32_t total = 2 * slot + 1024;
-    if (total + 1024 <= smem_max) {   // 1 KB left for static shared memory
-      if (out) *out = Tc2Layout{a, b, d, a_bufs, slot, total};
-      return true;
-    }
-  }
-  return false;
-}
-
-bool tc3_layout(int32_t k_steps, int32_t TL, int32_t stages, int32_t b_layout, Tc3Layout* out,
-                int32_t smem_max) {
-  if (256 + 2 * TL > 512 || TL > 128) return false;   // TMEM: S_0, S_1 (128 each) + O_0, O_1
-  int32_t a, b, d;
-  tc_smem_bytes(k_steps, 128, TL, stages, b_layout, &a, &b, &d);
-  const int32_t q = std::max<int32_t>(a, 16384);
-  for (int32_t q_bufs = 2; q_bufs >= 1; --q_bufs) {
-    const int32_t bars = 8 * (4 + 3 * stages + 5);
-    const int32_t total = q_bufs * 2 * q + stages * (b + d) + bars + 1024;
-    if (total + 1024 <= smem_max) {
-      if (out) *out = Tc3Layout{q, b, d, q_bufs, total};
-      return true;
-    }
-  }
-  return false;
-}
-
 bool tc4_layout(int32_t k_steps, int32_t TL, int32_t stages, int32_t b_layout, Tc4Layout* out,
                 int32_t smem_max) {
   if (TL > 128 || k_steps < 1) return false;   // TMEM: NSB S buffers + O_0, O_1
@@ -122,6 +87,24 @@ bool tc4_layout(int32_t k_steps, int32_t TL, int32_t stages, int32_t b_layout, T
   for (int32_t q_bufs = 2; q_bufs >= 1; --q_bufs) {
     const int32_t bars = 8 * (18 + 2 * stages);
     const int32_t total = q_bufs * 2 * a + stages * (b + d) + bars + 1024;
+    if (total + 5120 <= smem_max) {   // 4 KB of (l, m) + slack stay for static shared memory
+      if (out) *out = Tc4Layout{a, b, d, q_bufs, total};
+      return true;
+    }
+  }
+  return false;
+}
+
+bool tc5_layout(int32_t k_steps, int32_t TL, int32_t stages, int32_t b_layout, Tc4Layout* out,
+                int32_t smem_max) {
+  // TMEM: S_0, S_1 (128 columns) + P_0, P_1 (64) + O_0, O_1 (64) = 512 columns, so L <= 64
+  if (TL > 64 || k_steps < 1 || stages < 2) return false;
+  int32_t a, b, d;
+  tc_smem_bytes(k_steps, 128, TL, stages, b_layout, &a, &b, &d);
+  for (int32_t q_bufs = 2; q_bufs >= 1; --q_bufs) {
+    const int32_t bars = 8 * (20 + 2 * stages);
+    const int32_t e_stage = 16384;   // E staging for the TMA-store epilogue (128 rows x 128 B)
+    const int32_t total = q_bufs * 2 * a + stages * (b + d) + e_stage + bars + 1024;
     if (total + 5120 <= smem_max) {   // 4 KB of (l, m) + slack stay for static shared memory
       if (out) *out = Tc4Layout{a, b, d, q_bufs, total};
       return true;
@@ -148,10 +131,9 @@ bool tc_eligible(const mbci_chain_desc_t& d) {
   return true;
 }
 
-// Round-1 measurement: kernels 0, 2 and 3 run ~2.2-2.6x slower than the roofline-style score
-// below (C2 24.3 vs 9.3 us, C3 79 vs 35 us); kernel 4 is scored from its measured per-tile cost.
-// The common factor keeps the two kinds of score comparable (the ranking inside 0/2/3 is
-// unchanged by it).
+// Round-1 measurement: kernel 0 runs ~2.2-2.6x slower than the roofline-style score below
+// (C2 24.3 vs 9.3 us); the persistent kernels 4 and 5 are scored from their measured per-tile
+// cost.  The common factor keeps the two kinds of score comparable.
 constexpr double kModelToB200 = 2.4;
 
 static void score_b200(const mbci_chain_desc_t& d, const mbci_hw_t& hw, mbci_plan_t& p) {
@@ -173,7 +155,7 @@ static void score_b200(const mbci_chain_desc_t& d, const mbci_hw_t& hw, mbci_pla
     t_tc = b * 2.0 * d.M * d.N * (d.K + d.L) / (hw.n_sm * 256.0 * hw.clock_hz);
     t_issue = t_tc;
   }
-  if (p.kernel == 4) {
+  if (p.kernel == 4 || p.kernel == 5) {
     // persistent pair units dealt round-robin (ceil(units / n_sm) rounds per SM).
     const int64_t units = b == 0 ? 0 : static_cast<int64_t>(b) * cdiv(d.M, 256);
     const int64_t ntm = std::max<int64_t>(1, nt);
@@ -182,24 +164,22 @@ static void score_b200(const mbci_chain_desc_t& d, const mbci_hw_t& hw, mbci_pla
     const bool halves = rem > 0 && 2 * rem <= hw.n_sm && ntm % 2 == 0 && d.mask == MBCI_MASK_NONE &&
                         p.stages >= (p.TL <= 64 ? 4 : 3);
     const int64_t tail_tiles = rem > 0 ? (halves ? ntm / 2 : ntm) : 0;
-    // Calibrated on B200 (round-1 traces, tools/trace_chain4.py): one 256 x 128 score tile of a
-    // pair unit costs ~0.75 us + 6 ns per unit of (K + L) (d = 64: 1.5 us, d = 128: 2.3 us) on an
-    // SM, plus ~3 us of prologue / epilogue per launch.
-    // NONE / SCALE (no exponentials): the issuer and tensor pipe bound the tile, ~half the cost.
-    const double t_pair = (d.op == MBCI_OP_SOFTMAX ? 0.75e-6 + 6.0e-9 * static_cast<double>(p.TK + p.TL)
-                                                   : 0.15e-6 + 4.0e-9 * static_cast<double>(p.TK + p.TL)) *
-                          (1.965e9 / hw.clock_hz);
+    // Calibrated on B200 (tools/trace_chain4.py): one 256 x 128 score tile of a pair unit costs
+    // (kernel 4) ~0.75 us + 6 ns per unit of (K + L) (d = 64: 1.5 us, d = 128: 2.3 us) on an SM,
+    // (kernel 5, separate P) ~0.35 us + 5 ns per unit of (K + L) (d = 64: 1.0 us), plus ~3 us of
+    // prologue / epilogue per launch (~2 us with programmatic dependent launch, kernel 5).
+    // NONE / SCALE (no exponentials): the issuer and tensor pipe bound the tile.
+    const double kd = static_cast<double>(p.TK + p.TL);
+    double t_pair;
+    if (p.kernel == 4)
+      t_pair = d.op == MBCI_OP_SOFTMAX ? 0.75e-6 + 6.0e-9 * kd : 0.15e-6 + 4.0e-9 * kd;
+    else
+      t_pair = d.op == MBCI_OP_SOFTMAX ? 0.35e-6 + 5.0e-9 * kd : 0.12e-6 + 3.0e-9 * kd;
+    t_pair *= 1.965e9 / hw.clock_hz;
+    const double fixed = p.kernel == 5 ? 2.0e-6 : 3.0e-6;
     // (ties go to the deeper ring, up to the 4 stages that keep two Q buffers at d = 64)
-    p.t_b200 = std::max(t_hbm, static_cast<double>(rounds * ntm + tail_tiles) * t_pair) + 3.0e-6 - 1e-12 * std::min<int32_t>(p.stages, 4);
-    return;
-  }
-  if (p.kernel == 2 || p.kernel == 3) {
-    // persistent stream-K: work splits evenly over 2 x n_sm slots; one prologue, no waves
-    const double units = static_cast<double>(p.n_block);
-    const double tiles = units * static_cast<double>(nt);
-    // slots differ by at most one tile; a slot holding < 1 tile of work idles the rest
-    const double qq = std::min(2.0, 1.0 + 2.0 * hw.n_sm / std::max(1.0, tiles));
-    p.t_b200 = (std::max(std::max(t_hbm, t_tc), std::max(t_sfu, t_issue)) * qq + 1.5e-6) * kModelToB200;
+    p.t_b200 = std::max(t_hbm, static_cast<double>(rounds * ntm + tail_tiles) * t_pair) + fixed -
+               1e-12 * std::min<int32_t>(p.stages, 4);
     return;
   }
   int32_t occ = 1;
@@ -217,6 +197,17 @@ static void score_b200(const mbci_chain_desc_t& d, const mbci_hw_t& hw, mbci_pla
   p.t_b200 = (std::max(std::max(t_hbm, t_tc), std::max(t_sfu, t_issue)) * q + t_fixed) * kModelToB200;
 }
 
+static void fill_model(const mbci_chain_desc_t& d, const mbci_hw_t& hw, int32_t s, mbci_plan_t& p) {
+  double t[5];
+  model_terms(d.batch, d.M, d.N, d.K, d.L, p.BM, p.BN, p.TK, p.TL, s, hw, t);
+  p.t_mem = t[0];
+  p.t_comp = t[1];
+  p.alpha = t[2];
+  p.t_estm = t[3];
+  p.n_block = static_cast<int64_t>(t[4]);
+  score_b200(d, hw, p);
+}
+
 int enumerate_plans(const mbci_chain_desc_t& d, const mbci_hw_t& hw,
                     std::vector<mbci_plan_t>& out, bool rule3) {
   out.clear();
@@ -224,84 +215,43 @@ int enumerate_plans(const mbci_chain_desc_t& d, const mbci_hw_t& hw,
   if (tc_eligible(d)) {
     const int32_t k_steps = static_cast<int32_t>(cdiv(d.K, 16));
     const int32_t lpad = static_cast<int32_t>(std::max<int64_t>(16, cdiv(d.L, 16) * 16));
-    for (int pass = 0; pass < 2 && out.empty(); ++pass) {
+    // Persistent families (kernels 5 and 4): one 128-key tile per step with the ragged last
+    // tile masked and only the L real columns stored, so Rule 3's padding waste
+    // does not apply to them; they need K >= 1 (a live G1) and N >= 1.
+    if (k_steps >= 1 && d.N >= 1) {
+      for (int kern : {5, 4}) {
+        for (int32_t st = 2; st <= 8; ++st) {
+          Tc4Layout lay;
+          const bool ok = kern == 5 ? tc5_layout(k_steps, lpad, st, d.b_layout, &lay, hw.smem_max)
+                                    : tc4_layout(k_steps, lpad, st, d.b_layout, &lay, hw.smem_max);
+          if (!ok) continue;
+          mbci_plan_t p{};
+          p.kernel = kern;
+          p.BM = 256;
+          p.BN = 128;
+          p.TK = 16 * k_steps;
+          p.TL = lpad;
+          p.stages = st;
+          p.smem_bytes = lay.smem_total;
+          p.tmem_cols = 512;
+          fill_model(d, hw, s, p);
+          out.push_back(p);
+        }
+      }
+    }
+    // Kernel 0 (one CTA per 128-row m tile and h chunk; also the K = 0 chain): the paper's
+    // space of BN and TL with Rule 3 (skipped if it rejects every tile, R17).
+    const size_t n0 = out.size();
+    for (int pass = 0; pass < 2 && out.size() == n0; ++pass) {
       const bool apply_rule3 = rule3 && (pass == 0);
       for (int32_t BN : {64, 128}) {
         if (apply_rule3 && d.N > 0 && rule3_reject(d.N, BN)) continue;
         for (int32_t TL = 16; TL <= lpad; TL += 16) {
           if (apply_rule3 && d.L > 0 && rule3_reject(d.L, TL)) continue;
           if (2 * BN + TL > hw.tmem_cols) continue;  // TMEM budget
-          for (int32_t st = 2; st <= 8 && BN == 128 && TL == lpad && k_steps >= 1 &&
-                               d.N >= 1; ++st) {
-            Tc4Layout lay4;
-            if (tc4_layout(k_steps, TL, st, d.b_layout, &lay4, hw.smem_max)) {
-              mbci_plan_t p{};
-              p.kernel = 4;
-              p.BM = 256;
-              p.BN = 128;
-              p.TK = 16 * k_steps;
-              p.TL = TL;
-              p.stages = st;
-              p.smem_bytes = lay4.smem_total;
-              p.tmem_cols = 512;
-              double t[5];
-              model_terms(d.batch, d.M, d.N, d.K, d.L, p.BM, p.BN, p.TK, p.TL, s, hw, t);
-              p.t_mem = t[0];
-              p.t_comp = t[1];
-              p.alpha = t[2];
-              p.t_estm = t[3];
-              p.n_block = static_cast<int64_t>(t[4]);
-              score_b200(d, hw, p);
-              out.push_back(p);
-            }
-          }
-          for (int32_t st = 2; st <= 8 && BN == 128; ++st) {
-            Tc3Layout lay3;
-            if (tc3_layout(k_steps, TL, st, d.b_layout, &lay3, hw.smem_max)) {
-              mbci_plan_t p{};
-              p.kernel = 3;
-              p.BM = 256;
-              p.BN = 128;
-              p.TK = std::max<int32_t>(16, 16 * k_steps);
-              p.TL = TL;
-              p.stages = st;
-              p.smem_bytes = lay3.smem_total;
-              p.tmem_cols = 512;
-              double t[5];
-              model_terms(d.batch, d.M, d.N, d.K, d.L, p.BM, p.BN, p.TK, p.TL, s, hw, t);
-              p.t_mem = t[0];
-              p.t_comp = t[1];
-              p.alpha = t[2];
-              p.t_estm = t[3];
-              p.n_block = static_cast<int64_t>(t[4]);
-              score_b200(d, hw, p);
-              out.push_back(p);
-            }
-          }
-          for (int32_t st = 2; st <= 8; ++st) {
-            Tc2Layout lay;
-            if (BN == 64 && tc2_layout(k_steps, BN, TL, st, d.b_layout, &lay, hw.smem_max)) {
-              mbci_plan_t p{};
-              p.kernel = 2;
-              p.BM = 128;
-              p.BN = BN;
-              p.TK = std::max<int32_t>(16, 16 * k_steps);
-              p.TL = TL;
-              p.stages = st;
-              p.smem_bytes = lay.smem_total;
-              p.tmem_cols = 512;
-              double t[5];
-              model_terms(d.batch, d.M, d.N, d.K, d.L, p.BM, p.BN, p.TK, p.TL, s, hw, t);
-              p.t_mem = t[0];
-              p.t_comp = t[1];
-              p.alpha = t[2];
-              p.t_estm = t[3];
-              p.n_block = static_cast<int64_t>(t[4]);
-              score_b200(d, hw, p);
-              out.push_back(p);
-            }
-          }
           for (int32_t st = 2; st <= 4; ++st) {
+            const int64_t smem = tc_smem_bytes(k_steps, BN, TL, st, d.b_layout, nullptr, nullptr, nullptr);
+            if (smem > hw.smem_max) continue;  // exact SMEM budget (Rule 4 on sm_100)
             mbci_plan_t p{};
             p.kernel = 0;
             p.BM = 128;
@@ -309,19 +259,9 @@ int enumerate_plans(const mbci_chain_desc_t& d, const mbci_hw_t& hw,
             p.TK = std::max<int32_t>(16, 16 * k_steps);
             p.TL = TL;
             p.stages = st;
-            const int64_t smem = tc_smem_bytes(k_steps, BN, TL, st, d.b_layout, nullptr, nullptr,
-                                               nullptr);
-            if (smem > hw.smem_max) continue;  // exact SMEM budget (Rule 4 on sm_100)
             p.smem_bytes = static_cast<int32_t>(smem);
             p.tmem_cols = tmem_alloc_cols(BN, TL);
-            double t[5];
-            model_terms(d.batch, d.M, d.N, d.K, d.L, p.BM, p.BN, p.TK, p.TL, s, hw, t);
-            p.t_mem = t[0];
-            p.t_comp = t[1];
-            p.alpha = t[2];
-            p.t_estm = t[3];
-            p.n_block = static_cast<int64_t>(t[4]);
-            score_b200(d, hw, p);
+            fill_model(d, hw, s, p);
             out.push_back(p);
           }
         }

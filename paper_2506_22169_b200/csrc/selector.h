@@ -16,24 +16,15 @@ int64_t tc_smem_bytes(int32_t k_steps, int32_t BN, int32_t TL, int32_t stages, i
 int32_t tmem_alloc_cols(int32_t BN, int32_t TL);
 bool tc_eligible(const mbci_chain_desc_t& d);
 
-// SMEM carve-up of the persistent two-slot kernel (chain_tc2.cuh).
-struct Tc2Layout {
-  int32_t a_bytes, b_stage, d_stage, a_bufs, slot_bytes, smem_total;
-};
-bool tc2_layout(int32_t k_steps, int32_t BN, int32_t TL, int32_t stages, int32_t b_layout, Tc2Layout* out,
-                int32_t smem_max = 232448);
-// SMEM carve-up of the two-Q-tile kernel (chain_tc3.cuh): Q pair buffers + B/D ring.
-struct Tc3Layout {
-  int32_t q_bytes, b_stage, d_stage, q_bufs, smem_total;
-};
-bool tc3_layout(int32_t k_steps, int32_t TL, int32_t stages, int32_t b_layout, Tc3Layout* out,
-                int32_t smem_max = 232448);
 // SMEM carve-up of the persistent ping-pong attention kernel (chain_tc4.cuh): Q pair buffers,
 // a K/V ring, barriers (l and the TMEM slot live in static shared memory).
 struct Tc4Layout {
   int32_t q_bytes, b_stage, d_stage, q_bufs, smem_total;
 };
 bool tc4_layout(int32_t k_steps, int32_t TL, int32_t stages, int32_t b_layout, Tc4Layout* out,
+                int32_t smem_max = 232448);
+// Kernel 5 (chain_tc5.cuh, L <= 64): the same SMEM carve-up with 20 + 2·stages barriers.
+bool tc5_layout(int32_t k_steps, int32_t TL, int32_t stages, int32_t b_layout, Tc4Layout* out,
                 int32_t smem_max = 232448);
 // rule3 = false skips Rule 3 entirely: an explicitly forced plan only has to be
 // legal (SMEM / TMEM / TMA), not preferred.

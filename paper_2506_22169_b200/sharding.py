@@ -59,3 +59,21 @@ def gather_rows(local, group=None):
     out = torch.empty((world * local.shape[0],) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
     dist.all_gather_into_tensor(out, local.contiguous(), group=group)
     return out
+
+
+def gather_shards(local, counts, group=None):
+    """All-gather per-rank tensors whose dim-0 sizes differ (strong scaling of a batch that does
+    not divide evenly): pad to the largest shard, gather, and concatenate the real rows in rank
+    order.  Checking only, never timed."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()):
+        return local
+    world = dist.get_world_size(group)
+    assert len(counts) == world and local.shape[0] == counts[dist.get_rank(group)]
+    mx = max(counts)
+    pad = torch.zeros((mx,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    pad[: local.shape[0]] = local
+    out = torch.empty((world * mx,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    dist.all_gather_into_tensor(out, pad.contiguous(), group=group)
+    return torch.cat([out[r * mx: r * mx + counts[r]] for r in range(world)], dim=0)

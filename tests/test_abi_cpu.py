@@ -112,25 +112,23 @@ def test_enumerated_plans_are_legal_and_scored(m, shape, b_layout):
     if any(x % 8 for x in (K, b_inner, L)):        # TMA needs 16-byte row strides
         assert [p.kernel for p in plans] == [1]
         return
-    assert {p.kernel for p in plans} <= {0, 2, 3, 4}
+    assert {p.kernel for p in plans} <= {0, 4, 5}
     for p in plans:
-        assert p.kernel in (0, 2, 3, 4) and p.BN in (64, 128)
-        assert p.BM == (256 if p.kernel in (3, 4) else 128)   # kernels 3, 4: two 128-row Q tiles per CTA
-        if p.kernel == 4:    # softmax only, whole L in the CTA
+        assert p.kernel in (0, 4, 5) and p.BN in (64, 128)
+        assert p.BM == (256 if p.kernel in (4, 5) else 128)   # kernels 4, 5: two 128-row Q tiles per CTA
+        if p.kernel in (4, 5):    # whole L in the CTA, 128-key tiles
             assert p.TL == lpad and p.BN == 128
+        if p.kernel == 5:         # S_0, S_1 + P_0, P_1 + O_0, O_1 in 512 TMEM columns
+            assert p.TL <= 64
         assert p.TL % 16 == 0 and 16 <= p.TL <= lpad
         assert p.TK == max(16, math.ceil(K / 16) * 16)
         assert p.smem_bytes <= hw.smem_max
         if p.kernel == 0:    # one CTA pipeline: S double-buffered + O
             assert 2 * p.BN + p.TL <= p.tmem_cols <= 512 and p.tmem_cols & (p.tmem_cols - 1) == 0
-        elif p.kernel == 2:  # two slots of 256 columns: S double-buffered + O each
-            assert p.tmem_cols == 512 and 2 * p.BN + p.TL <= 256
-        else:                # two Q tiles: S_0, S_1 (128 each) + O_0, O_1
-            assert p.tmem_cols == 512 and p.BN == 128 and 256 + 2 * p.TL <= 512
+        else:
+            assert p.tmem_cols == 512 and p.smem_bytes + 5120 <= hw.smem_max
         assert 2 <= p.stages <= (4 if p.kernel == 0 else 8)
-        if p.kernel == 4:
-            assert p.smem_bytes + 5120 <= hw.smem_max
-        if rule3_ok:
+        if rule3_ok and p.kernel == 0:   # kernels 4 / 5 mask ragged key tiles: exempt from Rule 3
             assert not model.rule3_reject(N, p.BN)
         ref = model.chain_estimate(b, M, N, K, L, p.BM, p.BN, p.TK, p.TL, 2, hw.W, hw.P, hw.n_sm)
         assert p.t_estm == pytest.approx(ref["t_estm"], rel=1e-12)
@@ -147,7 +145,7 @@ def test_bert_base_prefers_full_L_tile(m):
     d = m.make_desc(96, 512, 512, 64, 64, "f16", "softmax")
     p = m.mbci_plan_t()
     assert m.mbci_plan_select(ctypes.byref(d), None, ctypes.byref(p)) == m.MBCI_OK
-    assert p.TL == 64 and p.kernel in (0, 4)
+    assert p.TL == 64 and p.kernel in (0, 4, 5)
 
 
 def test_fp32_and_misaligned_go_to_cuda_cores(m):
@@ -166,30 +164,46 @@ def test_rule3_fallback_keeps_a_plan_on_ragged_N(m):
     assert all(model.rule3_reject(300, p.BN) for p in plans)
 
 
-def test_kernel4_plans_for_attention_shapes(m):
-    """Kernel 4 (persistent ping-pong) is the default for 16-bit chains of every op; its plans use
-    the whole L per CTA, 128-key tiles, fit SMEM with room for the static (l, m) arrays, and the
-    4-stage plan (which enables half items for the last partial round) ranks first on C2."""
+def test_persistent_plans_for_attention_shapes(m):
+    """Kernel 5 (separate P) is the default for 16-bit chains with L <= 64 and kernel 4 for
+    64 < L <= 128, for every op; their plans use the whole L per CTA, 128-key tiles, fit SMEM
+    with room for the static (l, m) arrays, and the 4-stage plan (which enables half items for
+    the last partial round) ranks first on C2."""
     hw = m.hw_default()
     for op in ("softmax", "scale", "none"):
         d = m.make_desc(96, 512, 512, 64, 64, "f16", op, 0.125)
         st, plans = m.plan_enumerate(d, hw)
-        assert st == m.MBCI_OK and plans[0].kernel == 4
+        assert st == m.MBCI_OK and plans[0].kernel == 5
     d = m.make_desc(96, 512, 512, 64, 64, "f16", "softmax", 0.125)
     st, plans = m.plan_enumerate(d, hw)
-    k4 = [p for p in plans if p.kernel == 4]
-    assert k4[0].stages == 4 and all(p.stages >= 3 for p in k4)
-    by_stages = {p.stages: p.t_b200 for p in k4}
-    assert by_stages[4] < by_stages[3]          # half items (stages >= 4) halve the tail round
-    for p in k4:
-        assert p.BN == 128 and p.TL == 64 and p.BM == 256 and p.tmem_cols == 512
-        assert p.smem_bytes + 5120 <= hw.smem_max
+    for kern in (4, 5):
+        kp = [p for p in plans if p.kernel == kern]
+        assert kp[0].stages == 4
+        assert all(p.stages >= (3 if kern == 4 else 2) for p in kp)
+        by_stages = {p.stages: p.t_b200 for p in kp}
+        assert by_stages[4] < by_stages[3]          # half items (stages >= 4) halve the tail round
+        for p in kp:
+            assert p.BN == 128 and p.TL == 64 and p.BM == 256 and p.tmem_cols == 512
+            assert p.smem_bytes + 5120 <= hw.smem_max
     # key padding disables half items: the 3- and 4-stage plans then score alike
     d = m.make_desc(96, 512, 512, 64, 64, "f16", "softmax", 0.125, mask=True)
     st, plans = m.plan_enumerate(d, hw)
-    k4 = {p.stages: p.t_b200 for p in plans if p.kernel == 4}
-    assert abs(k4[4] - k4[3]) < 1e-9
-    # d = 128 (C5 shape): two S buffers, a 2-deep ring is the only fit with the Q pair
+    k5 = {p.stages: p.t_b200 for p in plans if p.kernel == 5}
+    assert abs(k5[4] - k5[3]) < 1e-9
+    # d = 128 (C5 shape): kernel 4 with two S buffers; a 2-deep ring is the only fit with the Q pair
     d = m.make_desc(512, 4096, 4096, 128, 128, "bf16", "softmax", 0.125)
     st, plans = m.plan_enumerate(d, hw)
     assert plans[0].kernel == 4 and plans[0].stages == 2 and plans[0].TL == 128
+    assert not any(p.kernel == 5 for p in plans)
+
+
+@pytest.mark.parametrize("N", [192, 320, 448, 576, 960, 1000, 512])
+def test_persistent_kernel_default_on_any_N(m, N):
+    """Rule 3 prunes kernel 0's BN only: the persistent kernels mask the ragged
+    last 128-key tile, so an odd multiple of 64 (or any N) keeps them as the default."""
+    st, plans = m.plan_enumerate(m.make_desc(96, 512, N, 64, 64, "f16", "softmax", 0.125))
+    assert st == m.MBCI_OK and plans[0].kernel == 5
+    st, plans = m.plan_enumerate(m.make_desc(512, 512, N, 128, 128, "bf16", "softmax", 0.125))
+    assert st == m.MBCI_OK and plans[0].kernel == 4
+    st, plans = m.plan_enumerate(m.make_desc(4, 256, N, 128, 128, "bf16", "softmax", 0.125))
+    assert {4, 0} <= {p.kernel for p in plans}     # a candidate even where kernel 0 ranks first

@@ -83,11 +83,16 @@ def test_ops_and_head_dims(mbci, op, K, L):
                                      (128, 130, 8, 8)])
 @pytest.mark.parametrize("b_layout", [0, 1])
 def test_ragged_shapes(mbci, M, N, K, L, b_layout):
-    if b_layout == 0 and N % 8:
-        pytest.skip("packed B[K,N] with N % 8 != 0 is not TMA-legal (CUDA-core path covers it)")
+    """Shapes that are not multiples of the tiles.  Packed B[K,N] with N % 8 != 0 has a row
+    stride that is not a 16-B multiple (not TMA-legal): the selector must fall back to the
+    CUDA-core kernel, which is checked against the oracle like every other path."""
     inp = gen.make_chain_inputs(M + N, "f16", 2, M, N, K, L, b_layout)
-    check(mbci, inp, "softmax", 1.0 / math.sqrt(K))
+    _, ch = check(mbci, inp, "softmax", 1.0 / math.sqrt(K))
     check(mbci, inp, "none", 1.0, budget=False)
+    if b_layout == 0 and N % 8:
+        assert ch.plan().kernel == 1, ch.describe()
+    elif K % 8 == 0 and L % 8 == 0 and not (b_layout == 1 and K % 8):
+        assert ch.plan().kernel != 1, ch.describe()
 
 
 def test_key_padding_mask(mbci):
@@ -168,7 +173,7 @@ def test_misaligned_pointer_rejected(mbci):
 
 
 # ------------------------------------------------------------------ strides
-@pytest.mark.parametrize("kernel", [0, 2, 3])
+@pytest.mark.parametrize("kernel", [0, 4, 5])
 def test_strided_operands(mbci, kernel):
     """Rows padded (ld > inner) and batch strides with gaps, 16-B multiples (TMA-legal),
     on every tensor-core kernel family."""
@@ -186,7 +191,7 @@ def test_strided_operands(mbci, kernel):
                to_dev(pad(inp.D, ldD, bsD), "f16"))
     E = torch.full((b * bsE,), float("nan"), dtype=torch.float16, device="cuda")
     pl = mbci.mbci_plan_t()
-    pl.kernel, pl.BN, pl.TL, pl.stages = kernel, (64 if kernel == 2 else 128), 48, 2
+    pl.kernel, pl.BN, pl.TL, pl.stages = kernel, 128, 48, (2 if kernel == 0 else 4)
     ch = mbci.Chain(b, M, N, K, L, "f16", "softmax", 0.125, b_layout=1, plan=pl,
                     strides=dict(ld_a=ldA, bs_a=bsA, ld_b=ldB, bs_b=bsB, ld_d=ldD, bs_d=bsD, ld_e=ldE, bs_e=bsE))
     assert ch.plan().kernel == kernel
@@ -252,22 +257,50 @@ def _sample_rows(batch, M, n, seed):
     return rows.astype(np.int64)
 
 
-@pytest.mark.parametrize("cfg", [
+FULL_CONFIGS = [
     ("C2", "f16", 96, 512, 512, 64, 64),
     ("C3", "bf16", 128, 1024, 1024, 64, 64),
     ("C4-16", "bf16", 64, 2048, 2048, 16, 16),
+    ("C4-32", "bf16", 64, 2048, 2048, 32, 32),
+    ("C4-64", "bf16", 64, 2048, 2048, 64, 64),
     ("C4-128", "bf16", 64, 2048, 2048, 128, 128),
+    ("C5", "bf16", 512, 4096, 4096, 128, 128),
     ("C6", "f16", 96, 256, 256, 64, 64),
-])
+]
+
+
+@pytest.mark.parametrize("cfg", FULL_CONFIGS, ids=[c[0] for c in FULL_CONFIGS])
 def test_full_size_configs_sampled(mbci, cfg):
+    """BASELINE.json configs at full size, default plan (the one bench.py times): 256 sampled
+    (β, m) rows, including the first and last β and row, each computed by the oracle alone."""
     name, dtype, b, M, N, K, L = cfg
     op = "none" if name.startswith("C4") else "softmax"
     sig = (1.0, 1.0 / math.sqrt(K), 1.0 / math.sqrt(N)) if op == "none" else (1.0, 1.0, 1.0)
-    inp = gen.make_chain_inputs(0, dtype, b, M, N, K, L, 1, sigmas=sig)
-    sc = 1.0 / math.sqrt(K)
+    inp = gen.make_chain_inputs(0, dtype, b, M, N, K, L, 1 if op == "softmax" else 0, sigmas=sig)
+    sc = 1.0 / math.sqrt(K) if op == "softmax" else 1.0
     E, ch = run_chain(mbci, inp, op, sc)
+    assert ch.plan().kernel != 1, ch.describe()
     rows = _sample_rows(b, M, 256, 1)
     ref = oracle.chain(inp, op, sc, rows=rows)
-    got = e_f64(E, dtype)[rows[:, 0], rows[:, 1]]
+    ix = torch.from_numpy(rows).to(E.device)
+    got = e_f64(E[ix[:, 0], ix[:, 1]], dtype)
     err = oracle.row_max_error(got, ref)
+    assert np.all(np.isfinite(got))
     assert err <= BUDGET[dtype], (name, err, ch.describe())
+
+
+def test_shard_is_bitwise_slice_of_full_run(mbci):
+    """rank r of g owns β in [r·b/g, (r+1)·b/g).  With the plan pinned, a shard's E
+    (inputs generated for batch_start = lo only) equals those rows of the unsharded run bit for bit."""
+    from paper_2506_22169_b200 import sharding
+    b, M, N, K, L = 24, 512, 512, 64, 64
+    full = gen.make_chain_inputs(3, "f16", b, M, N, K, L, 1)
+    E_full, ch = run_chain(mbci, full, "softmax", 0.125)
+    pin = ch.plan()
+    for r, g in ((1, 2), (3, 4), (7, 8)):
+        lo, hi = sharding.shard_range(b, r, g)
+        part = gen.make_chain_inputs(3, "f16", hi - lo, M, N, K, L, 1, batch_start=lo)
+        assert np.array_equal(part.A, full.A[lo:hi]) and np.array_equal(part.D, full.D[lo:hi])
+        E_part, ch2 = run_chain(mbci, part, "softmax", 0.125, plan=pin)
+        assert ch2.plan().kernel == pin.kernel
+        assert torch.equal(E_part.view(torch.int16), E_full[lo:hi].view(torch.int16)), (r, g, ch2.describe())

@@ -1,5 +1,7 @@
-"""Parity of kernel family 4 (chain_tc4.cuh: persistent ping-pong attention kernel) with the fp64
-oracle, forced through mbci_chain_create_with_plan so every case runs that kernel.
+"""Parity of the persistent ping-pong kernels with the fp64 oracle: kernel 4 (chain_tc4.cuh, P
+aliasing S, any L <= 128) and kernel 5 (chain_tc5.cuh, separate P buffers, L <= 64), each forced
+through mbci_chain_create_with_plan so every case runs that kernel (cases with L > 64 skip
+kernel 5).
 
 Covers: both B layouts and dtypes, head dims 16..128 (d = 128 single-buffers Q), ragged M
 (a pair unit whose second 128-row tile is entirely past M), ragged N and K/L not multiples of
@@ -39,17 +41,32 @@ def emu(request, monkeypatch):
     return request.param
 
 
-def k4_plan(mbci, L, stages=None):
-    if stages is None:   # three S buffers (TL <= 64) need a 3-deep K/V ring; d = 128 fits only 2
+_KERN = {"k": 4}
+
+
+@pytest.fixture(autouse=True, params=[4, 5], ids=["k4", "k5"])
+def kern(request):
+    _KERN["k"] = request.param
+    yield request.param
+
+
+def k4_plan(mbci, L, stages=None, K=64):
+    """Plan of the kernel under test (fixture `kern`) for head dims K, L."""
+    k = _KERN["k"]
+    if k == 5 and L > 64:
+        pytest.skip("kernel 5 keeps S_0, S_1, P_0, P_1, O_0, O_1 in TMEM: L <= 64")
+    if stages is None:   # kernel 4, TL <= 64: three S buffers need a 3-deep ring; d = 128 fits only 2
         stages = 3 if L <= 64 else 2
+        if k == 5 and K > 64:   # two 64-column Q / K chunks and the E staging: a 2-deep ring fits
+            stages = 2
     p = mbci.mbci_plan_t()
-    p.kernel, p.BN, p.TL, p.stages = 4, 128, max(16, (L + 15) // 16 * 16), stages
+    p.kernel, p.BN, p.TL, p.stages = k, 128, max(16, (L + 15) // 16 * 16), stages
     return p
 
 
 def check4(mbci, inp, scale, valid_len=None, stages=None, rows=None):
-    E, ch = run_chain(mbci, inp, "softmax", scale, valid_len, plan=k4_plan(mbci, inp.L, stages))
-    assert ch.plan().kernel == 4, ch.describe()
+    E, ch = run_chain(mbci, inp, "softmax", scale, valid_len, plan=k4_plan(mbci, inp.L, stages, inp.K))
+    assert ch.plan().kernel == _KERN["k"], ch.describe()
     got = e_f64(E, inp.dtype)
     if rows is not None:
         ref = oracle.chain(inp, "softmax", scale, valid_len=valid_len, rows=rows)
@@ -190,7 +207,7 @@ def test_k4_strided_operands(mbci):
     E = torch.full((b * bsE,), float("nan"), dtype=torch.float16, device="cuda")
     ch = mbci.Chain(b, M, N, K, L, "f16", "softmax", 0.125, b_layout=1, plan=k4_plan(mbci, L),
                     strides=dict(ld_a=ldA, bs_a=bsA, ld_b=ldB, bs_b=bsB, ld_d=ldD, bs_d=bsD, ld_e=ldE, bs_e=bsE))
-    assert ch.plan().kernel == 4
+    assert ch.plan().kernel == _KERN["k"]
     ch.run(A, B, D, E)
     torch.cuda.synchronize()
     Ef = E.cpu().float().numpy().astype(np.float64).reshape(b, bsE)
@@ -208,8 +225,8 @@ def test_k4_plain_chain_integer_bitwise(mbci, dtype, K, b_layout):
     RN-even(oracle E) bit for bit (SURVEY §8(c) pin), for NONE and SCALE (0.5)."""
     inp = gen.make_chain_inputs(200 + K, dtype, 3, 384, 640, K, K, b_layout, kind="int")
     for op, sc in (("none", 1.0), ("scale", 0.5)):
-        E, ch = run_chain(mbci, inp, op, sc, plan=k4_plan(mbci, K))
-        assert ch.plan().kernel == 4, ch.describe()
+        E, ch = run_chain(mbci, inp, op, sc, plan=k4_plan(mbci, K, K=K))
+        assert ch.plan().kernel == _KERN["k"], ch.describe()
         ref = oracle.chain(inp, op, sc)
         assert np.array_equal(e_bits(E), rn_bits(ref, dtype)), ch.describe()
 
@@ -219,7 +236,7 @@ def test_k4_plain_chain_ragged(mbci, M, N, K, L):
     sig = (1.0, 1.0 / math.sqrt(K), 1.0 / math.sqrt(N))
     inp = gen.make_chain_inputs(M + N + 7, "bf16", 2, M, N, K, L, 1, sigmas=sig)
     for op, sc in (("none", 1.0), ("scale", -0.75)):
-        E, ch = run_chain(mbci, inp, op, sc, plan=k4_plan(mbci, L))
+        E, ch = run_chain(mbci, inp, op, sc, plan=k4_plan(mbci, L, K=K))
         err = oracle.row_max_error(e_f64(E, "bf16"), oracle.chain(inp, op, sc))
         assert err <= BUDGET["bf16"], (op, err, ch.describe())
 

@@ -234,6 +234,23 @@ def test_phi_goldens():
     assert round(model.phi_printed(256, 256, 1)) == 1
 
 
+def test_is_memory_bound_examples():
+    """PAPER.md:119 (§II-A): MBCI iff φ < P/W (strict).  SPEC.md:76-79 examples: threshold 100
+    flops per element, φ = 204.8 → compute-bound, φ = 0.996 → memory-bound, φ == P/W →
+    compute-bound."""
+    W = 1.0e12
+    P = 100.0 * W   # P / W = 100
+    assert not model.is_memory_bound(model.phi_printed(256, 256, 1024), P, W)
+    assert model.is_memory_bound(model.phi_printed(256, 256, 1), P, W)
+    assert not model.is_memory_bound(100.0, P, W)
+    assert model.is_memory_bound(math.nextafter(100.0, 0.0), P, W)
+    # §I's narrative (PAPER.md:78): K 1024 → 1 moves a 256-tile MatMul across any threshold
+    # between the two ratios, e.g. A100's FP16 ridge 312e12 / 1.555e12 ≈ 200.6 flops per byte
+    ridge = 312e12 / 1.555e12
+    assert not model.is_memory_bound(model.phi_text(256, 256, 1024), ridge, 1.0)
+    assert model.is_memory_bound(model.phi_text(256, 256, 1), ridge, 1.0)
+
+
 def test_fused_intensity_independent_of_K_L():
     for K, L in ((16, 16), (64, 64), (128, 32)):
         assert model.fused_intensity(512, 512, K, L, 2) == pytest.approx(256.0)
