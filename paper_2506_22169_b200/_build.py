@@ -9,12 +9,15 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmbci.so")
 LIB_TRACE = os.path.join(HERE, "libmbci_trace.so")
-SOURCES = [os.path.join(CSRC, "api.cu"), os.path.join(CSRC, "selector.cpp")]
+# api.cu (ABI + host logic), selector.cpp, and one translation unit per kernel family / dtype
+# (k_*.cu), compiled in parallel and linked into one shared library.
+SOURCES = [os.path.join(CSRC, "api.cu"), os.path.join(CSRC, "selector.cpp")] + sorted(
+    os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.startswith("k_") and f.endswith(".cu"))
 DEPS = SOURCES + [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith((".cuh", ".h"))] + [
     os.path.join(os.path.dirname(HERE), "include", "mbci.h")]
 
 NVCC_FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
-              "-Xcompiler", "-fPIC", "-shared"]
+              "-Xcompiler", "-fPIC"]
 
 
 def nvcc() -> str:
@@ -42,8 +45,19 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False) -> st
     lib = LIB_TRACE if trace else LIB
     if force or stale_lib(lib):
         extra = ["-DMBCI_TRACE=1"] if trace else []
-        cmd = [nvcc()] + NVCC_FLAGS + extra + (["-Xptxas", "-v"] if verbose else []) + ["-o", lib + ".tmp"] + SOURCES
-        subprocess.check_call(cmd)
+        objdir = os.path.join(HERE, "build", "trace" if trace else "release")
+        os.makedirs(objdir, exist_ok=True)
+        objs, procs = [], []
+        for src in SOURCES:
+            obj = os.path.join(objdir, os.path.basename(src) + ".o")
+            objs.append(obj)
+            cmd = [nvcc()] + NVCC_FLAGS + extra + (["-Xptxas", "-v"] if verbose else []) + ["-c", "-o", obj, src]
+            procs.append((src, subprocess.Popen(cmd)))
+        failed = [src for src, pr in procs if pr.wait() != 0]
+        if failed:
+            raise RuntimeError("nvcc failed for " + ", ".join(os.path.basename(f) for f in failed))
+        subprocess.check_call([nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", lib + ".tmp"]
+                              + objs)
         os.replace(lib + ".tmp", lib)
     return lib
 

@@ -15,10 +15,8 @@
 #include <vector>
 
 #include "../../include/mbci.h"
-#include "chain_simt.cuh"
-#include "chain_tc.cuh"
-#include "chain_tc4.cuh"
-#include "chain_tc5.cuh"
+#include "chain_tc5.cuh"   // kT5Threads (the kernels are instantiated in k_*.cu)
+#include "kernels.h"
 #include "selector.h"
 
 using namespace mbci;
@@ -82,70 +80,6 @@ mbci_status_t normalize(const mbci_chain_desc_t* in, mbci_chain_desc_t* d) {
 int64_t span_elems(int64_t batch, int64_t rows, int64_t cols, int64_t ld, int64_t bs) {
   if (batch == 0 || rows == 0 || cols == 0) return 0;
   return (batch - 1) * bs + (rows - 1) * ld + cols;
-}
-
-using TcKernel = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, TcParams);
-
-template <bool BF16, int BN, int KCH, int BL>
-TcKernel pick_d(int dch) {
-  return dch == 1 ? (TcKernel)k_chain_tc<BF16, BN, KCH, BL, 1> : (TcKernel)k_chain_tc<BF16, BN, KCH, BL, 2>;
-}
-template <bool BF16, int BN, int KCH>
-TcKernel pick_bl(int bl, int dch) {
-  return bl == 0 ? pick_d<BF16, BN, KCH, 0>(dch) : pick_d<BF16, BN, KCH, 1>(dch);
-}
-template <bool BF16, int BN>
-TcKernel pick_kch(int kch, int bl, int dch) {
-  return kch == 1 ? pick_bl<BF16, BN, 1>(bl, dch) : pick_bl<BF16, BN, 2>(bl, dch);
-}
-template <bool BF16>
-TcKernel pick_bn(int bn, int kch, int bl, int dch) {
-  return bn == 64 ? pick_kch<BF16, 64>(kch, bl, dch) : pick_kch<BF16, 128>(kch, bl, dch);
-}
-TcKernel pick_tc(bool bf16, int bn, int kch, int bl, int dch) {
-  return bf16 ? pick_bn<true>(bn, kch, bl, dch) : pick_bn<false>(bn, kch, bl, dch);
-}
-
-using Tc4Kernel = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, Tc4Params);
-template <bool BF16, int KCH, int BL, int DCH>
-Tc4Kernel pick4_emu(int emu) {
-  constexpr int NSB = DCH == 1 ? 3 : 2;   // three S buffers fit TMEM next to two 64-column O
-  switch (emu) {
-    case 0: return (Tc4Kernel)k_chain_tc4<BF16, KCH, BL, DCH, 0, NSB>;
-    case 2: return (Tc4Kernel)k_chain_tc4<BF16, KCH, BL, DCH, 2, NSB>;
-    default: return (Tc4Kernel)k_chain_tc4<BF16, KCH, BL, DCH, 3, NSB>;
-  }
-}
-template <bool BF16, int KCH, int BL>
-Tc4Kernel pick4_d(int dch, int emu) {
-  return dch == 1 ? pick4_emu<BF16, KCH, BL, 1>(emu) : pick4_emu<BF16, KCH, BL, 2>(emu);
-}
-template <bool BF16, int KCH>
-Tc4Kernel pick4_bl(int bl, int dch, int emu) {
-  return bl == 0 ? pick4_d<BF16, KCH, 0>(dch, emu) : pick4_d<BF16, KCH, 1>(dch, emu);
-}
-Tc4Kernel pick_tc4(bool bf16, int kch, int bl, int dch, int emu) {
-  if (bf16) return kch == 1 ? pick4_bl<true, 1>(bl, dch, emu) : pick4_bl<true, 2>(bl, dch, emu);
-  return kch == 1 ? pick4_bl<false, 1>(bl, dch, emu) : pick4_bl<false, 2>(bl, dch, emu);
-}
-
-using Tc5Kernel = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, Tc4Params);
-template <bool BF16, int KCH, int BL>
-Tc5Kernel pick5_emu(int emu) {
-  switch (emu) {
-    case 0: return (Tc5Kernel)k_chain_tc5<BF16, KCH, BL, 0>;
-    case 2: return (Tc5Kernel)k_chain_tc5<BF16, KCH, BL, 2>;
-    case 4: return (Tc5Kernel)k_chain_tc5<BF16, KCH, BL, 4>;
-    default: return (Tc5Kernel)k_chain_tc5<BF16, KCH, BL, 3>;
-  }
-}
-template <bool BF16, int KCH>
-Tc5Kernel pick5_bl(int bl, int emu) {
-  return bl == 0 ? pick5_emu<BF16, KCH, 0>(emu) : pick5_emu<BF16, KCH, 1>(emu);
-}
-Tc5Kernel pick_tc5(bool bf16, int kch, int bl, int emu) {
-  if (bf16) return kch == 1 ? pick5_bl<true, 1>(bl, emu) : pick5_bl<true, 2>(bl, emu);
-  return kch == 1 ? pick5_bl<false, 1>(bl, emu) : pick5_bl<false, 2>(bl, emu);
 }
 
 // Kernel-5 feature flags (Tc4Params::flags); MBCI_T5_FLAGS overrides (diagnostics).
@@ -350,9 +284,7 @@ mbci_status_t setup_plan(mbci_chain* h) {
   } else {
     if (d.batch * d.M > INT32_MAX) return fail(MBCI_ERR_UNSUPPORTED, "batch * M exceeds the CUDA-core grid");
     p.n_block = d.batch * d.M;
-    const void* fn = d.dtype == MBCI_F32 ? (const void*)k_chain_simt<float>
-                     : d.dtype == MBCI_F16 ? (const void*)k_chain_simt<__half>
-                                           : (const void*)k_chain_simt<__nv_bfloat16>;
+    const void* fn = simt_fn((int)d.dtype);
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_bytes);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
   }
@@ -457,16 +389,8 @@ mbci_status_t launch(mbci_chain* h, const void* A, const void* B, const void* D,
     sp.ld_a = d.ld_a; sp.ld_b = d.ld_b; sp.ld_d = d.ld_d; sp.ld_e = d.ld_e;
     sp.bs_a = d.bs_a; sp.bs_b = d.bs_b; sp.bs_d = d.bs_d; sp.bs_e = d.bs_e;
     const unsigned grid = (unsigned)(d.batch * d.M);
-    const int smem = h->plan.smem_bytes;
-    if (d.dtype == MBCI_F32)
-      k_chain_simt<float><<<grid, kSimtThreads, smem, st>>>((const float*)A, (const float*)B,
-                                                             (const float*)D, (float*)E, sp);
-    else if (d.dtype == MBCI_F16)
-      k_chain_simt<__half><<<grid, kSimtThreads, smem, st>>>((const __half*)A, (const __half*)B,
-                                                              (const __half*)D, (__half*)E, sp);
-    else
-      k_chain_simt<__nv_bfloat16><<<grid, kSimtThreads, smem, st>>>(
-          (const __nv_bfloat16*)A, (const __nv_bfloat16*)B, (const __nv_bfloat16*)D, (__nv_bfloat16*)E, sp);
+    cudaError_t le = launch_simt((int)d.dtype, grid, h->plan.smem_bytes, st, A, B, D, E, sp);
+    if (le != cudaSuccess) return cuda_fail(le, "CUDA-core kernel launch");
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "kernel launch");

@@ -40,6 +40,11 @@
 // written by one TMA bulk tensor store per 128-row tile (per-thread 16-B global stores from
 // the epilogue warps stretched the softmax warps' MUFU phases ~2x on the shared MIO queue).
 //
+// P_x hand-off: the softmax computes a step's exponentials into registers and waits for G2 of the
+// previous step (p_free) only before writing P_x, so the exp phase overlaps that G2 and its
+// issue latency (the wait-first order put P stored -> issuer wake -> G2 -> p_free on every
+// step's critical path).  A lazy rescale of O_x still waits first.
+//
 // Programmatic dependent launch: every CTA lets the next grid of the stream be scheduled at
 // once (griddepcontrol.launch_dependents) and waits for its prerequisite grids before its
 // first global-memory access (griddepcontrol.wait), so barrier initialisation, TMEM
@@ -60,15 +65,17 @@ constexpr int kT5Threads = 512;
 
 // t4_exp_row (chain_tc4.cuh) with the exp-phase hand-over folded in: after chunk `arrive_after`
 // (of 4 chunks of 16 column pairs) the other slot's warp of this SMSP may start its turn
-// (bar != 0), so the two warps overlap on the MUFU for the remaining chunks.
+// (bar != 0), so the two warps overlap on the MUFU for the remaining chunks.  The packed 16-bit
+// P row stays in registers (`pk`, 64 words: the S registers die as the pairs are consumed) and is
+// written to TMEM by the caller once G2 of the previous step has released P_x — so the
+// exponentials of step g overlap G2(g - 1) instead of waiting for it.
 template <bool BF16, int EMU, bool MASKED>
-__device__ __forceinline__ void t5_exp_row(uint32_t tP, const uint32_t (&sr)[kT4BN], float sc, float m, int valid,
-                                           float2& l2a, float2& l2b, int arrive_after, uint32_t bar) {
+__device__ __forceinline__ void t5_exp_row(uint32_t (&pk)[64], const uint32_t (&sr)[kT4BN], float sc, float m,
+                                           int valid, float2& l2a, float2& l2b, int arrive_after, uint32_t bar) {
   const float2 sc2 = make_float2(sc, sc);
   const float2 nm2 = make_float2(-m, -m);
 #pragma unroll
   for (int ch = 0; ch < 4; ++ch) {
-    uint32_t pk[16];
 #pragma unroll
     for (int c = 0; c < 16; ++c) {
       const int cp = ch * 16 + c;
@@ -85,11 +92,16 @@ __device__ __forceinline__ void t5_exp_row(uint32_t tP, const uint32_t (&sr)[kT4
         e.y = (2 * cp + 1 < valid) ? e.y : 0.f;
       }
       if (c & 1) l2b = __fadd2_rn(l2b, e); else l2a = __fadd2_rn(l2a, e);
-      pk[c] = ptx::pack2<BF16>(e.x, e.y);
+      pk[cp] = ptx::pack2<BF16>(e.x, e.y);
     }
-    ptx::tmem_st16(tP + ch * 16, pk);
     if (bar != 0 && ch == arrive_after) ptx::named_bar_arrive(bar, 64);
   }
+}
+
+// P_x <- the packed row (64 columns of 16-bit pairs), 16 columns per tcgen05.st
+__device__ __forceinline__ void t5_store_p(uint32_t tP, const uint32_t (&pk)[64]) {
+#pragma unroll
+  for (int ch = 0; ch < 4; ++ch) ptx::tmem_st16(tP + ch * 16, &pk[ch * 16]);
 }
 
 template <bool BF16, int KCH, int BL, int EMU>
@@ -265,7 +277,6 @@ __global__ void __launch_bounds__(kT5Threads, 1)
           int kst;
           uint32_t kph;
           c1.entry(x, S, kst, kph);
-          if (tr && !(p.dbg & 16) && c1.g < kT4TrTiles) tr[T4TR(c1.g, 12 + x)] = t4_clk();
           wait1(&kv_full[kst], kph);
           ptx::tc_fence_after();
           const uint32_t q_lo = (sQ0 + (c1.qb * 2 + (c1.hf ? 0 : x)) * p.q_bytes) >> 4;   // half: one Q tile
@@ -280,11 +291,7 @@ __global__ void __launch_bounds__(kT5Threads, 1)
             }
           }
           ptx::mma_commit(&s_full[x]);
-          if (tr && c1.g < kT4TrTiles) tr[T4TR(c1.g, 10 + x)] = t4_clk();
-          if (tr && (p.dbg & 8) && c1.g < kT4TrTiles) {   // trace build: G1 completion probe
-            ptx::mbar_spin(&s_full[x], c1.g & 1);
-            tr[T4TR(c1.g, 6 + x)] = t4_clk();
-          }
+          if (tr && c1.g < kT4TrTiles) tr[T4TR(c1.g, 14 + x)] = t4_clk();
           if (c1.j == c1.nt - 1) ptx::mma_commit(&q_empty[c1.qb]);   // this slot's last read of Q
           c1.advance(p, G);
         };
@@ -295,9 +302,8 @@ __global__ void __launch_bounds__(kT5Threads, 1)
             wait1(&s_free[x], ph);   // softmax x has S(x, step c2) in registers
             issue_g1();
           }
-          if (tr && !(p.dbg & 8) && c2.g < kT4TrTiles) tr[T4TR(c2.g, 14 + x)] = t4_clk();
           wait1(&p_full[x], ph);
-          if (tr && !(p.dbg & 8) && c2.g < kT4TrTiles) tr[T4TR(c2.g, 6 + x)] = t4_clk();
+          if (tr && c2.g < kT4TrTiles) tr[T4TR(c2.g, 10 + x)] = t4_clk();
           if (c2.j == 0 && c2.ai > 0) wait1(&o_free[x], (c2.ai - 1) & 1);
           ptx::tc_fence_after();
           int vst;
@@ -309,11 +315,7 @@ __global__ void __launch_bounds__(kT5Threads, 1)
           for (int ks = 0; ks < kT4BN / 16; ++ks)
             ptx::mma_ts(tO, tP + ks * 8, dD + v_lo + ks * 128, idesc2, ks > 0 ? 1u : acc0);
           ptx::mma_commit(&p_free[x]);
-          if (tr && c2.g < kT4TrTiles) tr[T4TR(c2.g, 8 + x)] = t4_clk();
-          if (tr && (p.dbg & 8) && c2.g < kT4TrTiles) {   // trace build: G2 completion probe
-            ptx::mbar_spin(&p_free[x], c2.g & 1);
-            tr[T4TR(c2.g, 14 + x)] = t4_clk();
-          }
+          if (tr && c2.g < kT4TrTiles) tr[T4TR(c2.g, 12 + x)] = t4_clk();
           // kv_empty counts two arrivals: one per slot on a shared entry, or both from the one
           // slot that reads a half item's entry
           ptx::mma_commit(&kv_empty[vst]);
@@ -487,13 +489,24 @@ __global__ void __launch_bounds__(kT5Threads, 1)
             mx = sc >= 0.f ? t4_row_extreme<false, true>(sr, valid) : t4_row_extreme<true, true>(sr, valid);
           const float m_tile = mx * sc;
           if (tr && row == 0 && g < kT4TrTiles) tr[T4TR(g, 2 + x)] = t4_clk_after(__float_as_uint(mx));
-          // P_x (and, for a rescale, O_x) is free once G2_x(g - 1) completed
-          if (g > 0) ptx::mbar_wait(&p_free[x], ph ^ 1u);
-          ptx::tc_fence_after();
+          // P_x (and, for a rescale, O_x) is free once G2_x(g - 1) completed.  Without a rescale
+          // the wait is deferred until the exponentials are in registers (flags bit 3 restores
+          // the early wait, for A/B measurements).
+          bool p_ready = g == 0;
+          if (!p_ready && (p.flags & 8)) {
+            ptx::mbar_wait(&p_free[x], ph ^ 1u);
+            ptx::tc_fence_after();
+            p_ready = true;
+          }
           if (j == 0) {
             m_run = m_tile;
           } else if (__any_sync(0xffffffffu, m_tile > m_run + kT4Tau)) {
-            // warp-uniform (tcgen05.ld/st are warp-collective)
+            // warp-uniform (tcgen05.ld/st are warp-collective); O_x must hold G2_x(g - 1)
+            if (!p_ready) {
+              ptx::mbar_wait(&p_free[x], ph ^ 1u);
+              ptx::tc_fence_after();
+              p_ready = true;
+            }
             const float m_new = fmaxf(m_run, m_tile);
             const float alpha = ptx::ex2(m_run - m_new);
             l2.x *= alpha;
@@ -511,15 +524,22 @@ __global__ void __launch_bounds__(kT5Threads, 1)
             }
           }
           if (turns && (x == 1 || g > 0)) ptx::named_bar_sync(bar_mine, 64);
-          if (tr && (p.dbg & 16) && row == 0 && g < kT4TrTiles) tr[T4TR(g, 12 + x)] = t4_clk();   // exps start
+          if (tr && row == 0 && g < kT4TrTiles) tr[T4TR(g, 4 + x)] = t4_clk();   // exps start
           // the other slot's warp may start its turn after chunk turn_chunk of this one's
+          uint32_t pk[64];
           if (full)
-            t5_exp_row<BF16, EMU, false>(tP, sr, sc, m_run, valid, l2, l2b, turn_chunk, turns ? bar_other : 0u);
+            t5_exp_row<BF16, EMU, false>(pk, sr, sc, m_run, valid, l2, l2b, turn_chunk, turns ? bar_other : 0u);
           else
-            t5_exp_row<BF16, 0, true>(tP, sr, sc, m_run, valid, l2, l2b, turn_chunk, turns ? bar_other : 0u);
+            t5_exp_row<BF16, 0, true>(pk, sr, sc, m_run, valid, l2, l2b, turn_chunk, turns ? bar_other : 0u);
+          if (tr && row == 0 && g < kT4TrTiles) tr[T4TR(g, 6 + x)] = t4_clk();   // exps done
+          if (!p_ready) {
+            ptx::mbar_wait(&p_free[x], ph ^ 1u);
+            ptx::tc_fence_after();
+          }
+          t5_store_p(tP, pk);
         }
         ptx::tmem_wait_st();
-        if (tr && row == 0 && g < kT4TrTiles) tr[T4TR(g, 4 + x)] = t4_clk();
+        if (tr && row == 0 && g < kT4TrTiles) tr[T4TR(g, 8 + x)] = t4_clk();
         ptx::tc_fence_before();
         __syncwarp();
         if (lane0) ptx::mbar_arrive(&p_full[x]);

@@ -1,0 +1,52 @@
+"""Per-step timeline of kernel 5 (MBCI_LIB=trace loads libmbci_trace.so).  Per step g and slot x
+(softmax warps of SMSP 0, issuer threads): S ready, row max done, exp turn acquired, exps done,
+P stored, P seen by the issuer, G2 issued, G1 of step g issued; median over CTAs (us from CTA
+start, clock64 / SM_GHZ).   usage: MBCI_LIB=trace python tools/trace_k5.py [--shape b,M,N,K,L]"""
+import sys, math, argparse, os
+import numpy as np, torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import mbci_inputs as gen
+from paper_2506_22169_b200 import mbci
+ap = argparse.ArgumentParser()
+ap.add_argument("--plan", default="5:128:64:4")
+ap.add_argument("--shape", default="96,512,512,64,64")
+ap.add_argument("--dtype", default="f16")
+ap.add_argument("--op", default="softmax")
+ap.add_argument("--steps", type=int, default=8)
+a = ap.parse_args()
+b, M, N, K, L = map(int, a.shape.split(","))
+plan = mbci.mbci_plan_t()
+plan.kernel, plan.BN, plan.TL, plan.stages = map(int, a.plan.split(":"))
+inp = gen.make_chain_inputs(0, a.dtype, b, M, N, K, L, 1 if a.op == "softmax" else 0)
+dt = torch.float16 if a.dtype == "f16" else torch.bfloat16
+T = lambda x: torch.from_numpy(x.view(np.int16)).view(dt).cuda()
+A, B, D = T(inp.A), T(inp.B), T(inp.D)
+E = torch.empty(b, M, L, dtype=dt, device="cuda")
+ch = mbci.Chain(b, M, N, K, L, a.dtype, a.op, 1 / math.sqrt(K), b_layout=1 if a.op == "softmax" else 0, plan=plan)
+S = 512
+tr = torch.zeros(148 * S, dtype=torch.int64, device="cuda")
+for i in range(30): ch.run(A, B, D, E)
+torch.cuda.synchronize()
+ch.set_trace(tr); ch.run(A, B, D, E); torch.cuda.synchronize(); ch.set_trace(None)
+t = tr.cpu().numpy().reshape(148, S).astype(np.int64)
+t = t[t[:, 0] > 0]
+t0 = t[:, 0].min()
+print(ch.describe(), "ctas", len(t))
+print(f"kernel span {(t[:,3].max()-t0)/1000:.2f} us; CTA start spread {(t[:,0].max()-t0)/1000:.2f} us; "
+      f"setup {np.mean(t[:,1]-t[:,0])/1000:.2f} us; CTA durations mean {np.mean(t[:,3]-t[:,0])/1000:.2f} max {np.max(t[:,3]-t[:,0])/1000:.2f}")
+GHZ = float(os.environ.get("SM_GHZ", "1.965"))
+def d(c, rows=None):
+    tt = t if rows is None else t[rows]
+    v = tt[:, c]
+    ok = v > 0
+    return np.median(v[ok] - tt[ok, 4]) / GHZ / 1e3 if ok.mean() > 0.5 else float("nan")
+cols = [("S", 0), ("max", 2), ("turn", 4), ("expd", 6), ("Pst", 8), ("Pseen", 10), ("G2is", 12), ("G1is", 14)]
+nsteps = (t[:, 8 + 16 * np.arange(28)] > 0).sum(1)
+for label, rows in (("all CTAs", None), ("CTAs with the most steps", nsteps == nsteps.max()), ("CTAs with the fewest steps", nsteps == nsteps.min())):
+    print(f"--- {label} ({len(t) if rows is None else int(rows.sum())} CTAs)")
+    print("step  " + "  ".join(f"{n}{x:<1d}".rjust(6) for n, _ in cols for x in (0, 1)) + "   TMA")
+    for g in range(a.steps):
+        c = 8 + 16 * g
+        row = [d(c + k + x, rows) for _, k in cols for x in (0, 1)] + [d(460 + g, rows)]
+        print(f"{g:4d}  " + "  ".join(f"{v:6.2f}" for v in row))
+    print("epilogue per item: " + "  ".join(f"[{d(490+4*u, rows):.2f} {d(491+4*u, rows):.2f} {d(492+4*u, rows):.2f}]" for u in range(4)))
