@@ -4,6 +4,7 @@ from __future__ import annotations
 
 import os
 import subprocess
+import tempfile
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
@@ -45,7 +46,8 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False) -> st
     lib = LIB_TRACE if trace else LIB
     if force or stale_lib(lib):
         extra = ["-DMBCI_TRACE=1"] if trace else []
-        objdir = os.path.join(HERE, "build", "trace" if trace else "release")
+        # objects outside the repo: only the linked .so travels to the GPU box
+        objdir = os.path.join(tempfile.gettempdir(), "mbci_build", "trace" if trace else "release")
         os.makedirs(objdir, exist_ok=True)
         objs, procs = [], []
         for src in SOURCES:

@@ -15,7 +15,7 @@
 #include <vector>
 
 #include "../../include/mbci.h"
-#include "chain_tc5.cuh"   // kT5Threads (the kernels are instantiated in k_*.cu)
+#include "chain_tc6.cuh"   // kT5Threads, kT6Threads (the kernels are instantiated in k_*.cu)
 #include "kernels.h"
 #include "selector.h"
 
@@ -90,6 +90,27 @@ int t5_flags_default() {
               // bits 4-5: hand the turn over that many 16-pair chunks before the end
 }
 
+// Kernel-6 feature flags (MBCI_T6_FLAGS overrides): bit 0 exp-phase turns between the slots,
+// bit 4 hand the turn over one 16-pair chunk early, bit 2 spinning single-thread waits.
+int t6_flags_default() {
+  const char* e = getenv("MBCI_T6_FLAGS");
+  if (e) return atoi(e) & 0x3F;
+  return 1;
+}
+
+bool env_is(const char* name, const char* value) {
+  const char* e = getenv(name);
+  return e && strcmp(e, value) == 0;
+}
+
+// L2 prefetch budget per CTA of kernels 5 / 6 before the grid-dependency wait (MBCI_PF_KB
+// overrides, 0 disables).
+int pf_bytes_default() {
+  const char* e = getenv("MBCI_PF_KB");
+  if (e) return std::max(0, atoi(e)) * 1024;
+  return 128 * 1024;
+}
+
 // Programmatic dependent launch for kernel 5 (MBCI_PDL=0 disables it, for A/B measurements).
 bool pdl_enabled() {
   const char* e = getenv("MBCI_PDL");
@@ -155,7 +176,8 @@ struct mbci_chain {
   TcKernel tc = nullptr;
   TcParams tp{};
   Tc4Kernel tc4 = nullptr;   // kernel 4
-  Tc5Kernel tc5 = nullptr;   // kernel 5 (same parameter block, plus E's tensor map)
+  Tc5Kernel tc5 = nullptr;   // kernels 5 / 6 (same parameter block, plus E's tensor map)
+  int32_t threads = 0;       // block size of the persistent kernels
   Tc4Params tp4{};
   int32_t grid2 = 0;
   int32_t kch = 1, dch = 1;
@@ -212,10 +234,10 @@ mbci_status_t setup_plan(mbci_chain* h) {
     cudaError_t e = cudaFuncSetAttribute((const void*)h->tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          p.smem_bytes);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
-  } else if (p.kernel == 4 || p.kernel == 5) {
+  } else if (p.kernel == 4 || p.kernel == 5 || p.kernel == 6) {
     const int32_t k_steps = static_cast<int32_t>((d.K + 15) / 16);
     Tc4Layout lay;
-    const bool fits = p.kernel == 5 ? tc5_layout(k_steps, p.TL, p.stages, d.b_layout, &lay)
+    const bool fits = p.kernel >= 5 ? tc5_layout(k_steps, p.TL, p.stages, d.b_layout, &lay)
                                     : tc4_layout(k_steps, p.TL, p.stages, d.b_layout, &lay);
     if (k_steps < 1 || d.N < 1 || !fits)
       return fail(MBCI_ERR_UNSUPPORTED, "kernel-%d plan needs K, N >= 1 and must fit SMEM/TMEM", p.kernel);
@@ -227,9 +249,11 @@ mbci_status_t setup_plan(mbci_chain* h) {
     h->tc5 = nullptr;
     if (p.kernel == 5)
       h->tc5 = pick_tc5(d.dtype == MBCI_BF16, h->kch, d.b_layout, t4_emu_default());
+    else if (p.kernel == 6)
+      h->tc5 = pick_tc6(d.dtype == MBCI_BF16, h->kch, d.b_layout, t4_emu_default());
     else
       h->tc4 = pick_tc4(d.dtype == MBCI_BF16, h->kch, d.b_layout, h->dch, t4_emu_default());
-    const void* kfn = p.kernel == 5 ? (const void*)h->tc5 : (const void*)h->tc4;
+    const void* kfn = p.kernel >= 5 ? (const void*)h->tc5 : (const void*)h->tc4;
     Tc4Params& t = h->tp4;
     t = Tc4Params{};
     t.M = (int32_t)d.M; t.N = (int32_t)d.N; t.K = (int32_t)d.K; t.L = (int32_t)d.L;
@@ -273,11 +297,14 @@ mbci_status_t setup_plan(mbci_chain* h) {
     t.items = (int32_t)(halves ? t.half_from + 2 * rem : units);
     h->grid2 = (int32_t)std::max<int64_t>(1, std::min<int64_t>(n_sm, t.items));
     p.n_block = t.items;
-    t.flags = p.kernel == 5 ? t5_flags_default() : 0;
+    t.flags = p.kernel == 5 ? t5_flags_default() : (p.kernel == 6 ? t6_flags_default() : 0);
+    t.pf_bytes = p.kernel >= 5 ? pf_bytes_default() : 0;
+    t.burst = (p.kernel >= 5 && !env_is("MBCI_T5_BURST", "0")) ? 1 : 0;
+    h->threads = p.kernel == 6 ? kT6Threads : (p.kernel == 5 ? kT5Threads : kT4Threads);
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_bytes);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
     int occ = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, p.kernel == 5 ? kT5Threads : kT4Threads,
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, h->threads,
                                                       p.smem_bytes);
     if (e != cudaSuccess) return cuda_fail(e, "occupancy query");
     if (occ < 1) return fail(MBCI_ERR_UNSUPPORTED, "kernel-%d CTA does not fit on an SM", p.kernel);
@@ -303,7 +330,7 @@ mbci_status_t launch(mbci_chain* h, const void* A, const void* B, const void* D,
   if (d.mask == MBCI_MASK_KEY_PADDING && !valid_len)
     return fail(MBCI_ERR_INVALID, "mask KEY_PADDING needs valid_len");
   const int32_t* vl = d.mask == MBCI_MASK_KEY_PADDING ? valid_len : nullptr;
-  if (h->plan.kernel == 0 || h->plan.kernel == 4 || h->plan.kernel == 5) {
+  if (h->plan.kernel == 0 || h->plan.kernel >= 4) {
     if (!aligned16(E) || (d.N > 0 && !aligned16(D)) || (d.K > 0 && d.N > 0 && (!aligned16(A) || !aligned16(B))))
       return fail(MBCI_ERR_UNSUPPORTED, "tensor-core path needs 16-byte aligned A, B, D, E");
     // tensor maps (cached by pointer triple)
@@ -321,7 +348,7 @@ mbci_status_t launch(mbci_chain* h, const void* A, const void* B, const void* D,
       memset(&ent->tb, 0, sizeof(CUtensorMap));
       memset(&ent->td, 0, sizeof(CUtensorMap));
       memset(&ent->te, 0, sizeof(CUtensorMap));
-      const uint32_t bn_box = (h->plan.kernel == 4 || h->plan.kernel == 5) ? 128u : (uint32_t)h->plan.BN;
+      const uint32_t bn_box = h->plan.kernel >= 4 ? 128u : (uint32_t)h->plan.BN;
       if (d.K > 0 && d.N > 0) {
         s = encode3d(&ent->ta, A, bf16, d.K, d.M, d.batch, d.ld_a, d.bs_a, 128);
         if (s != MBCI_OK) return s;
@@ -336,7 +363,7 @@ mbci_status_t launch(mbci_chain* h, const void* A, const void* B, const void* D,
         s = encode3d(&ent->td, D, bf16, d.L, d.N, d.batch, d.ld_d, d.bs_d, bn_box);
         if (s != MBCI_OK) return s;
       }
-      if (h->plan.kernel == 5) {   // E: TMA bulk stores of 128-row x 64-column tiles
+      if (h->plan.kernel >= 5) {   // E: TMA bulk stores of 128-row x 64-column tiles
         s = encode3d(&ent->te, E, bf16, d.L, d.M, d.batch, d.ld_e, d.bs_e, 128);
         if (s != MBCI_OK) return s;
       }
@@ -365,7 +392,7 @@ mbci_status_t launch(mbci_chain* h, const void* A, const void* B, const void* D,
       t.trace = h->trace;
       cudaLaunchConfig_t cfg{};
       cfg.gridDim = dim3((unsigned)h->grid2);
-      cfg.blockDim = dim3(kT5Threads);
+      cfg.blockDim = dim3((unsigned)h->threads);
       cfg.dynamicSmemBytes = (size_t)h->plan.smem_bytes;
       cfg.stream = st;
       cudaLaunchAttribute attr[1];
@@ -374,7 +401,7 @@ mbci_status_t launch(mbci_chain* h, const void* A, const void* B, const void* D,
       cfg.attrs = attr;
       cfg.numAttrs = pdl_enabled() ? 1 : 0;
       cudaError_t le = cudaLaunchKernelEx(&cfg, h->tc5, ent->ta, ent->tb, ent->td, ent->te, t);
-      if (le != cudaSuccess) return cuda_fail(le, "kernel-5 launch");
+      if (le != cudaSuccess) return cuda_fail(le, "kernel-5/6 launch");
     }
   } else {
     SimtParams sp{};
@@ -564,7 +591,7 @@ mbci_status_t create_impl(const mbci_chain_desc_t* desc, int device, const mbci_
     // The shortlist keeps the best-ranked plans of every kernel family so that a model error
     // between families cannot hide the fastest kernel.
     std::vector<mbci_plan_t> shortlist;
-    for (int fam : {5, 4, 0, 1}) {
+    for (int fam : {6, 5, 4, 0, 1}) {
       int taken = 0;
       for (const auto& q : plans)
         if (q.kernel == fam && taken < 3) {
@@ -687,14 +714,14 @@ mbci_status_t mbci_chain_describe(mbci_chain_t h, char* buf, size_t len) {
   snprintf(buf, len,
            "kernel=%s BM=%d BN=%d TK=%d TL=%d stages=%d smem=%d tmem=%d n_block=%lld "
            "t_estm=%.3gs alpha=%.4f t_b200=%.3gs",
-           p.kernel == 0 ? "tcgen05" : (p.kernel == 4 ? "tcgen05-pingpong" : (p.kernel == 5 ? "tcgen05-pingpong-sepP" : "simt")), p.BM, p.BN, p.TK, p.TL, p.stages, p.smem_bytes, p.tmem_cols,
+           p.kernel == 0 ? "tcgen05" : (p.kernel == 4 ? "tcgen05-pingpong" : (p.kernel == 5 ? "tcgen05-pingpong-sepP" : (p.kernel == 6 ? "tcgen05-pingpong-splitrow" : "simt"))), p.BM, p.BN, p.TK, p.TL, p.stages, p.smem_bytes, p.tmem_cols,
            (long long)p.n_block, p.t_estm, p.alpha, p.t_b200);
   return MBCI_OK;
 }
 
 mbci_status_t mbci_chain_set_trace(mbci_chain_t h, void* buf, int64_t cap_bytes) {
   if (!h) return fail(MBCI_ERR_INVALID, "handle is NULL");
-  const int64_t need = (h->plan.kernel == 4 || h->plan.kernel == 5) ? (int64_t)h->grid2 * kT4TraceSlots * 8
+  const int64_t need = h->plan.kernel >= 4 ? (int64_t)h->grid2 * kT4TraceSlots * 8
                                              : h->plan.n_block * kTraceSlots * 8;
   if (buf && cap_bytes < need) return fail(MBCI_ERR_INVALID, "trace buffer needs %lld bytes", (long long)need);
   h->trace = static_cast<uint64_t*>(buf);

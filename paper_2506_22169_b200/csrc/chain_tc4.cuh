@@ -73,6 +73,8 @@ struct Tc4Params {
   uint64_t* trace;         // [gridDim.x][kT4TraceSlots] (MBCI_TRACE builds only)
   int32_t flags;           // kernel 5: bit 0 = exp-phase turns between the two slots' warps of an
                            // SMSP, bit 2 = issuer / TMA threads spin on test_wait (A/B only)
+  int32_t burst;           // kernels 5 / 6: 1 = the prologue issues only the first step's K/V entries
+  int32_t pf_bytes;        // kernels 5 / 6: L2 prefetch budget per CTA before the grid-dependency wait
   int32_t dbg;             // diagnostics only (MBCI_T4_DEBUG): 1 = softmax skips its TMEM/math work,
                            // 2 = issuer skips the G2 MMAs, 4 = issuer skips the G1 MMAs
 };

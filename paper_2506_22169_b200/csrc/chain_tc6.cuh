@@ -1,81 +1,48 @@
-// chain_tc5.cuh — persistent ping-pong fused chain E = op(A·B)·D on sm_100a, head dims <= 64,
-// with a separate P buffer per slot (the default kernel for L <= 64).
+// chain_tc6.cuh — kernel 6: kernel 5 (chain_tc5.cuh) with every score row split across TWO softmax
+// warps, so each SMSP runs four softmax warps instead of two.
 //
-// Same arithmetic and work layout as chain_tc4.cuh (mbci.h; PAPER.md:196 chain, :498 softmax
-// between the GEMMs, :489 batched layout; units = (β, pair of 128-row m tiles) bound to a
-// persistent grid, PAPER.md:285 Rule 1; k loop dead for K <= 128; S_E hoisted,
-// PAPER.md:232-233; half items for the last partial round).  What differs is the TMEM layout
-// and, from it, the dependency graph of a step:
+// Same arithmetic, work items, TMEM layout (S_0, S_1, P_0, P_1, O_0, O_1 = 512 columns), barrier
+// protocol and issuer / TMA / epilogue roles as kernel 5 (PAPER.md:196 chain, :498 softmax
+// between the GEMMs, :489 batched layout; Rule 1 spatial loops on the persistent grid, :285; dead
+// k loop, :253; S_E hoisted, :232-233).  What differs is the softmax:
 //
-//   kernel 4 (d <= 64):  three 128-column S buffers rotated over both slots, P aliasing S.  The
-//     next S tile of slot x can only be written once the OTHER slot's G2 has read the P that
-//     occupies the buffer, so a slot's next score tile waits for p_full(1-x) -> G2 -> G1 ->
-//     s_full: ~0.5 us of every 1.5 us step on C2 (round-2 trace, profiles/r2_SUMMARY.md).
-//   kernel 5:  S_0, S_1 (128 columns each), P_0, P_1 (64 columns of packed 16-bit P each),
-//     O_0, O_1 (64 columns each) = 512 columns.  S_x is released (s_free) as soon as softmax x
-//     has the row in registers, so G1(x, j+1) runs while softmax x computes the exponentials of
-//     tile j; P_x is released (p_free) by the commit after G2(x, j).  Each slot's chain only
-//     involves its own buffers, so the two slots no longer serialise each other.
+//   kernel 5: one warp per (slot, TMEM lane quadrant) owns a whole 128-column S row: 128 S
+//     registers, a 480-instruction unrolled exponential block, and per tile a ~460-cycle TMEM
+//     load during which that warp issues nothing.  Measured (round 2, profiles/r2_*): the exp
+//     phase of one warp ran at half its isolated rate, `no_instruction` (i-cache, L0 ~6 KB) was
+//     the top stall of the exp loop, and two warps per SMSP could not hide the TMEM latency.
+//   kernel 6: warps w and w + 8 (same SMSP, same lanes) share the rows of slot x = (w >> 2) & 1:
+//     half h = w >> 3 owns key columns [64h, 64h + 64) of each S tile.  Per tile each warp loads
+//     64 columns, takes its partial row max, swaps it with its partner through shared memory
+//     (one 64-thread named barrier per (slot, quadrant)), computes 64 exponentials (a 240-
+//     instruction block shared by all 16 warps) and writes its 32 packed P columns.  The two
+//     halves keep separate row sums, added by the epilogue; the lazy-rescale decision is
+//     identical in both (same combined row max), each rescales its half of O_x's 16-column
+//     chunks.
 //
-// One tcgen05 issuer thread per slot (warps 12 and 14), each in its own order, per step g:
-//     wait s_free(x, g) -> G1(x, g + 1) -> commit s_full(x)
-//     wait p_full(x, g) -> G2(x, g)     -> commit p_free(x) [+ kv_empty, o_full]
-// so neither slot's next score tile waits behind the other slot's hand-offs (a single issuer
-// serialising both slots cost ~0.45 us per step on C2: it blocked on the full MMA issue queue
-// after each G2 before it could issue the other slot's G1).  Deadlock-free: every wait is for
-// work whose own inputs were issued earlier in the same slot's order; a K/V entry is released
-// after both readers' commits (kv_empty counts 2), Q after both slots' last G1 (q_empty 2).
-//
-// Softmax: 8 warps, warp w serves slot x = w >> 2 and TMEM lane quadrant q = w & 3 (rows 32q ..
-// 32q + 31): a whole 128-column S row per thread in registers (setmaxnreg 184).  Exp-phase turns
-// (flags bit 0): warp w of slot 0 and warp w + 4 of slot 1 share SMSP q; their exponential
-// phases alternate (named barriers 1-4: slot 0's turn, 5-8: slot 1's), so the MUFU serves one
-// warp at a time while the other loads S and takes its row max.  In isolation one warp reaches
-// 14.5 ex2/clk/SM with 2/8 of the pairs on the FMA-pipe polynomial (tools/exp_sched_bench.cu).
-// The single-thread roles (issuers, TMA) wait with mbarrier.try_wait, which suspends the thread,
-// instead of spinning on test_wait: a spinning thread takes issue slots from the softmax warp of
-// its SMSP (flags bit 2 restores spinning, for A/B measurements).
-//
-// Epilogue (warps 8-11): E = O / l packed to 16 bits into a 128-B-swizzled shared tile and
-// written by one TMA bulk tensor store per 128-row tile (per-thread 16-B global stores from
-// the epilogue warps stretched the softmax warps' MUFU phases ~2x on the shared MIO queue).
-//
-// P_x hand-off: the softmax computes a step's exponentials into registers and waits for G2 of the
-// previous step (p_free) only before writing P_x, so the exp phase overlaps that G2 and its
-// issue latency (the wait-first order put P stored -> issuer wake -> G2 -> p_free on every
-// step's critical path).  A lazy rescale of O_x still waits first.
-//
-// Programmatic dependent launch: every CTA lets the next grid of the stream be scheduled at
-// once (griddepcontrol.launch_dependents) and waits for its prerequisite grids before its
-// first global-memory access (griddepcontrol.wait), so barrier initialisation, TMEM
-// allocation and descriptor prefetch of step i + 1 overlap the tail of step i.
-//
-// Warps: 0-7 softmax | 8-11 epilogue | 12 tcgen05 issuer of slot 0 + TMEM allocator | 13 TMA
-//        producer | 14 tcgen05 issuer of slot 1 | 15 idle.  setmaxnreg: 184 / 80 / 64.
+// Warps: 0-15 softmax (w & 3 = lane quadrant, (w >> 2) & 1 = slot, w >> 3 = column half) |
+//        16-19 epilogue | 20 tcgen05 issuer of slot 0 + TMEM allocator | 21 TMA producer |
+//        22 tcgen05 issuer of slot 1 | 23 idle.  768 threads; setmaxnreg 96 / 56 / 40.
 #pragma once
 #include "chain_tc4.cuh"
+#include "chain_tc5.cuh"
 
 namespace mbci {
 
-constexpr uint32_t kT5PCol = 256;   // P_0 at 256, P_1 at 320
-constexpr uint32_t kT5OCol = 384;   // O_0 at 384, O_1 at 448
+// 24 warps = 6 per SMSP, so ptxas gives every thread 80 registers at launch (the per-SMSP file
+// holds 512 per lane); setmaxnreg then moves them: 16 x 96 + 4 x 56 + 4 x 40 = 24 x 80.
+constexpr int kT6Threads = 768;
 
-constexpr uint32_t kT5EStage = 16384;   // E staging: 128 rows x 128 B (64 16-bit columns), 128-B swizzle
-constexpr int kT5Threads = 512;
-
-// t4_exp_row (chain_tc4.cuh) with the exp-phase hand-over folded in: after chunk `arrive_after`
-// (of 4 chunks of 16 column pairs) the other slot's warp of this SMSP may start its turn
-// (bar != 0), so the two warps overlap on the MUFU for the remaining chunks.  The packed 16-bit
-// P row stays in registers (`pk`, 64 words: the S registers die as the pairs are consumed) and is
-// written to TMEM by the caller once G2 of the previous step has released P_x — so the
-// exponentials of step g overlap G2(g - 1) instead of waiting for it.
+// p = 2^(sc·S − m) for the 64 scores of a half row (registers) into 32 packed 16-bit words `pk`,
+// two packed partial sums.  MASKED: columns >= valid give 0.  After chunk `arrive_after` (of 2
+// chunks of 16 pairs) the other slot's warps of this SMSP may start their exponentials (bar != 0).
 template <bool BF16, int EMU, bool MASKED>
-__device__ __forceinline__ void t5_exp_row(uint32_t (&pk)[64], const uint32_t (&sr)[kT4BN], float sc, float m,
-                                           int valid, float2& l2a, float2& l2b, int arrive_after, uint32_t bar) {
+__device__ __forceinline__ void t6_exp_half(uint32_t (&pk)[32], const uint32_t (&sr)[64], float sc, float m,
+                                            int valid, float2& l2a, float2& l2b, int arrive_after, uint32_t bar) {
   const float2 sc2 = make_float2(sc, sc);
   const float2 nm2 = make_float2(-m, -m);
 #pragma unroll
-  for (int ch = 0; ch < 4; ++ch) {
+  for (int ch = 0; ch < 2; ++ch) {
 #pragma unroll
     for (int c = 0; c < 16; ++c) {
       const int cp = ch * 16 + c;
@@ -94,61 +61,64 @@ __device__ __forceinline__ void t5_exp_row(uint32_t (&pk)[64], const uint32_t (&
       if (c & 1) l2b = __fadd2_rn(l2b, e); else l2a = __fadd2_rn(l2a, e);
       pk[cp] = ptx::pack2<BF16>(e.x, e.y);
     }
-    if (bar != 0 && ch == arrive_after) ptx::named_bar_arrive(bar, 64);
+    if (bar != 0 && ch == arrive_after) ptx::named_bar_arrive(bar, 128);
   }
 }
 
-// P_x <- the packed row (64 columns of 16-bit pairs), 16 columns per tcgen05.st
-__device__ __forceinline__ void t5_store_p(uint32_t tP, const uint32_t (&pk)[64]) {
+// NONE / SCALE: P = cvt(scale · S) for a 64-column half row
+template <bool BF16>
+__device__ __forceinline__ void t6_cvt_half(uint32_t tP, const uint32_t (&sr)[64], float sc) {
+  const float2 sc2 = make_float2(sc, sc);
 #pragma unroll
-  for (int ch = 0; ch < 4; ++ch) ptx::tmem_st16(tP + ch * 16, &pk[ch * 16]);
+  for (int ch = 0; ch < 2; ++ch) {
+    uint32_t pk[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+      const int cp = ch * 16 + c;
+      const float2 z = __fmul2_rn(make_float2(__uint_as_float(sr[2 * cp]), __uint_as_float(sr[2 * cp + 1])), sc2);
+      pk[c] = ptx::pack2<BF16>(z.x, z.y);
+    }
+    ptx::tmem_st16(tP + ch * 16, pk);
+  }
 }
 
-// L2 prefetch of this CTA's first items (Q tiles and every K/V tile they read), up to
-// p.pf_bytes, issued by the TMA thread BEFORE griddepcontrol.wait: with programmatic dependent
-// launch the CTA is resident while the previous grid drains, so the HBM latency of its first
-// loads overlaps that tail (L2 is coherent: the loads after the wait still see the previous
-// grid's writes).  Key padding is ignored here (valid_len may be written by the previous grid).
-template <int KCH, int BL>
-__device__ __forceinline__ void t5_prefetch_l2(const Tc4Params& p, const CUtensorMap* tmA, const CUtensorMap* tmB,
-                                               const CUtensorMap* tmD) {
-  int64_t bytes = 0;
-  const int ntv = (p.N + kT4BN - 1) / kT4BN;
-  for (int i = blockIdx.x; i < p.items && bytes < p.pf_bytes; i += gridDim.x) {
-    T4Item it;
-    it.decode(p, i);
-    const int beta = it.u / p.l_mp;
-    const int m0 = (it.u - beta * p.l_mp) * 256 + (it.half > 0 ? 128 : 0);
-    const int nq = (it.half < 0 && m0 + 128 < p.M) ? 2 : 1;
-    for (int x = 0; x < nq; ++x)
+// Extreme (max, or min for a negative scale) of a 64-column half row; MASKED: first `valid` only.
+template <bool MIN, bool MASKED>
+__device__ __forceinline__ float t6_half_extreme(const uint32_t (&sr)[64], int valid) {
+  if constexpr (MASKED) {
+    float mx = MIN ? INFINITY : -INFINITY;
 #pragma unroll
-      for (int c = 0; c < KCH; ++c) ptx::tma_prefetch_l2_3d(tmA, c * 64, m0 + x * 128, beta);
-    bytes += nq * p.q_bytes;
-    for (int t = 0; t < ntv && bytes < p.pf_bytes; ++t) {
-      if constexpr (BL == 1) {
-#pragma unroll
-        for (int c = 0; c < KCH; ++c) ptx::tma_prefetch_l2_3d(tmB, c * 64, t * kT4BN, beta);
-      } else {
-#pragma unroll
-        for (int c = 0; c < kT4BN / 64; ++c) ptx::tma_prefetch_l2_3d(tmB, t * kT4BN + c * 64, 0, beta);
-      }
-      ptx::tma_prefetch_l2_3d(tmD, 0, t * kT4BN, beta);
-      bytes += p.b_stage_bytes + p.d_stage_bytes;
+    for (int c = 0; c < 64; ++c) {
+      const float v = __uint_as_float(sr[c]);
+      if (c < valid) mx = MIN ? fminf(mx, v) : fmaxf(mx, v);
     }
+    return mx;
+  } else {
+    float a[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      a[q] = MIN ? fminf(__uint_as_float(sr[2 * q]), __uint_as_float(sr[2 * q + 1]))
+                 : fmaxf(__uint_as_float(sr[2 * q]), __uint_as_float(sr[2 * q + 1]));
+#pragma unroll
+    for (int c = 16; c < 64; c += 16)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) a[q] = t4_red<MIN>(a[q], __uint_as_float(sr[c + 2 * q]), __uint_as_float(sr[c + 2 * q + 1]));
+    return t4_red<MIN>(t4_red<MIN>(a[0], a[1], a[2]), t4_red<MIN>(a[3], a[4], a[5]), MIN ? fminf(a[6], a[7]) : fmaxf(a[6], a[7]));
   }
 }
 
 template <bool BF16, int KCH, int BL, int EMU>
-__global__ void __launch_bounds__(kT5Threads, 1)
-    k_chain_tc5(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+__global__ void __launch_bounds__(kT6Threads, 1)
+    k_chain_tc6(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmE,
                 const Tc4Params p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   __shared__ uint32_t tmem_base_slot;
-  __shared__ float l_sm[2][2][128];   // [slot][active-item parity][row]: row sum of p
-  __shared__ float m_sm[2][2][128];   // [slot][parity][row]: running max (log2) the p were taken against
+  __shared__ float l_sm[2][2][2][128];   // [slot][column half][active-item parity][row]: partial row sums
+  __shared__ float m_sm[2][2][128];      // [slot][parity][row]: running max (log2) the p were taken against
+  __shared__ float xmax[2][2][2][128];   // [tile parity][slot][column half][row]: partial row extremes
 
   const int S = p.stages;
   const uint32_t kv_stage = p.b_stage_bytes + p.d_stage_bytes;
@@ -160,20 +130,19 @@ __global__ void __launch_bounds__(kT5Threads, 1)
   uint64_t* q_empty = bars + 2;     // [2]
   uint64_t* o_full = bars + 4;      // [2] last G2_x of an item completed
   uint64_t* o_free = bars + 6;      // [2] epilogue read O_x (128 arrivals)
-  uint64_t* l_full = bars + 8;      // [2] softmax x published l (one arrival per warp: 4)
+  uint64_t* l_full = bars + 8;      // [2] softmax x published l (one arrival per warp: 8)
   uint64_t* l_free = bars + 10;     // [2] epilogue read l_sm[x][ai & 1] (128 arrivals)
   uint64_t* s_full = bars + 12;     // [2] G1_x landed in S_x (commit)
-  uint64_t* s_free = bars + 14;     // [2] softmax x holds S_x in registers (one arrival per warp: 4)
-  uint64_t* p_full = bars + 16;     // [2] softmax x wrote P_x (one arrival per warp: 4)
+  uint64_t* s_free = bars + 14;     // [2] softmax x holds S_x in registers (one arrival per warp: 8)
+  uint64_t* p_full = bars + 16;     // [2] softmax x wrote P_x (one arrival per warp: 8)
   uint64_t* p_free = bars + 18;     // [2] G2_x read P_x and updated O_x (commit)
   uint64_t* kv_full = bars + 20;    // [S] K_g and V_g landed
   uint64_t* kv_empty = kv_full + S; // [S] the G2s reading the entry completed (two commits)
 
   const int warp = threadIdx.x >> 5;
-  // Work-skipping diagnostics (MBCI_T4_DEBUG, trace build only; results are wrong by design):
-  // 1 softmax and 16 epilogue keep only their barrier protocol, 2 / 4 the issuers skip the G2 / G1
-  // MMAs (commits stay), 64 "TMA only": the issuers release each ring entry as soon as it lands
-  // and every other role idles, 128 the softmax ignores s_full / p_free (free-running, timing only).
+  // Diagnostics (trace build only): 256 = exp-throughput probe — every softmax warp runs its
+  // exponential block kProbeReps times on one S tile (with the exp-phase turns when enabled),
+  // 512 adds the per-tile TMEM load and row max; no other role works.  Results are garbage.
 #if MBCI_TRACE
   const int dbg = p.dbg;
 #else
@@ -219,17 +188,17 @@ __global__ void __launch_bounds__(kT5Threads, 1)
   // The TMA warp initialises the barriers; the first item's Q and ring entries go out before
   // the CTA-wide barrier (after the prerequisite grid completed), overlapping TMEM allocation.
   int pre_entries = 0;
-  if (warp == 13 && ptx::elect_one()) {
+  if (warp == 21 && !(dbg & 256) && ptx::elect_one()) {
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&q_full[i], 1);
       ptx::mbar_init(&q_empty[i], 2);   // each slot's issuer commits after its last G1
       ptx::mbar_init(&o_full[i], 1);
       ptx::mbar_init(&o_free[i], 128);
-      ptx::mbar_init(&l_full[i], 4);
+      ptx::mbar_init(&l_full[i], 8);
       ptx::mbar_init(&l_free[i], 128);
       ptx::mbar_init(&s_full[i], 1);
-      ptx::mbar_init(&s_free[i], 4);
-      ptx::mbar_init(&p_full[i], 4);
+      ptx::mbar_init(&s_free[i], 8);
+      ptx::mbar_init(&p_full[i], 8);
       ptx::mbar_init(&p_free[i], 1);
     }
     for (int s = 0; s < S; ++s) {
@@ -258,7 +227,7 @@ __global__ void __launch_bounds__(kT5Threads, 1)
       break;
     }
   }
-  if (warp == 12) ptx::tmem_alloc(&tmem_base_slot, 512);
+  if (warp == 20) ptx::tmem_alloc(&tmem_base_slot, 512);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -267,16 +236,16 @@ __global__ void __launch_bounds__(kT5Threads, 1)
   if (tr && threadIdx.x == 0) tr[1] = ptx::globaltimer();
   const int G = gridDim.x;
 
-  if (warp >= 12) {
-    ptx::setmaxnreg_dec<64>();
+  if (warp >= 20) {
+    ptx::setmaxnreg_dec<40>();
     // single-thread roles: try_wait (suspending) unless flags bit 2 asks for spinning
     const bool spin = (p.flags & 4) != 0;
     auto wait1 = [&](uint64_t* bar, uint32_t parity) {
       if (spin) ptx::mbar_spin(bar, parity); else ptx::mbar_wait(bar, parity);
     };
-    if (warp == 13) {
+    if (warp == 21) {
       // ============================================================ TMA producer
-      if (ptx::elect_one()) {
+      if (!(dbg & 256) && ptx::elect_one()) {
         int g = 0, ai = 0;   // g: ring entries used so far
         for (int i = blockIdx.x; i < p.items; i += G) {
           T4Item it;
@@ -302,10 +271,10 @@ __global__ void __launch_bounds__(kT5Threads, 1)
           }
         }
       }
-    } else if (warp == 12 || warp == 14) {
+    } else if (warp == 20 || warp == 22) {
       // ============================================================ tcgen05 issuers (one per slot)
-      if (ptx::elect_one()) {
-        const int x = warp == 12 ? 0 : 1;
+      if (!(dbg & 256) && ptx::elect_one()) {
+        const int x = warp == 20 ? 0 : 1;
         const uint64_t dA = ptx::sdesc_sw128(0, 16, 1024);
         const uint64_t dB = (BL == 1) ? ptx::sdesc_sw128(0, 16, 1024) : ptx::sdesc_sw128(0, p.kp_rows * 128, 1024);
         const uint64_t dD = ptx::sdesc_sw128(0, kT4BN * 128, 1024);
@@ -334,7 +303,7 @@ __global__ void __launch_bounds__(kT5Threads, 1)
               const uint64_t ad = dA + q_lo + (ks >> 2) * 1024 + (ks & 3) * 2;
               const uint64_t bd = (BL == 1) ? dB + k_lo + (ks >> 2) * (kT4BN * 8) + (ks & 3) * 2
                                             : dB + k_lo + ks * 128;
-              if (!(dbg & 4)) ptx::mma_ss(dS, ad, bd, idesc1, ks > 0 ? 1u : 0u);
+              ptx::mma_ss(dS, ad, bd, idesc1, ks > 0 ? 1u : 0u);
             }
           }
           ptx::mma_commit(&s_full[x]);
@@ -342,19 +311,6 @@ __global__ void __launch_bounds__(kT5Threads, 1)
           if (c1.j == c1.nt - 1) ptx::mma_commit(&q_empty[c1.qb]);   // this slot's last read of Q
           c1.advance(p, G);
         };
-        if (dbg & 64) {   // TMA only: release every entry of this slot as soon as it lands
-          for (; c1.valid; c1.advance(p, G)) {
-            if (c1.j == 0) wait1(&q_full[c1.qb], c1.qph);
-            int kst;
-            uint32_t kph;
-            c1.entry(x, S, kst, kph);
-            wait1(&kv_full[kst], kph);
-            ptx::mbar_arrive(&kv_empty[kst]);
-            if (c1.hf) ptx::mbar_arrive(&kv_empty[kst]);
-            if (c1.j == c1.nt - 1) ptx::mbar_arrive(&q_empty[c1.qb]);
-          }
-          c2.valid = false;
-        }
         if (c1.valid) issue_g1();
         uint32_t ph = 0;   // parity of step c2.g (s_free / p_full phases count this slot's steps)
         while (c2.valid) {
@@ -373,7 +329,7 @@ __global__ void __launch_bounds__(kT5Threads, 1)
           const uint32_t acc0 = c2.j > 0 ? 1u : 0u;
 #pragma unroll
           for (int ks = 0; ks < kT4BN / 16; ++ks)
-            if (!(dbg & 2)) ptx::mma_ts(tO, tP + ks * 8, dD + v_lo + ks * 128, idesc2, ks > 0 ? 1u : acc0);
+            ptx::mma_ts(tO, tP + ks * 8, dD + v_lo + ks * 128, idesc2, ks > 0 ? 1u : acc0);
           ptx::mma_commit(&p_free[x]);
           if (tr && c2.g < kT4TrTiles) tr[T4TR(c2.g, 12 + x)] = t4_clk();
           // kv_empty counts two arrivals: one per slot on a shared entry, or both from the one
@@ -386,25 +342,18 @@ __global__ void __launch_bounds__(kT5Threads, 1)
         }
       }
     }
-  } else if (warp >= 8) {
-    // ============================================================ epilogue (warps 8-11)
-    ptx::setmaxnreg_dec<80>();
-    const int row = threadIdx.x - 256;   // TMEM lane (warp 8+w reads lanes 32w..32w+31)
+  } else if (warp >= 16) {
+    // ============================================================ epilogue (warps 16-19)
+    ptx::setmaxnreg_dec<56>();
+    const int row = threadIdx.x - 512;   // TMEM lane (warp 16+w reads lanes 32w..32w+31)
     const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
-    const bool leader = threadIdx.x == 256;
+    const bool leader = threadIdx.x == 512;
     const uint32_t sE0 = ptx::smem_u32(sE) + row * 128;
     int ai = 0;
     // E tile (beta, rows gm0 .. gm0 + 127) = w0·O_0 + w1·O_1 (one slot: w1 = 0), packed to 16
     // bits into the 128-B-swizzled staging tile, then one TMA bulk tensor store (clipped to L
     // columns and M rows by the tensor map).  O is released (o_free) once read.
     auto emit = [&](int beta, int gm0, int x0, float w0, int x1, float w1, int nt) {
-      if (dbg & 16) {
-        if (nt > 0) {
-          ptx::mbar_arrive(&o_free[x0]);
-          if (x1 >= 0) ptx::mbar_arrive(&o_free[x1]);
-        }
-        return;
-      }
       if (leader) ptx::tma_store_wait_read();   // the previous store has read the staging
       ptx::named_bar_sync(9, 128);
       const uint32_t tA = tmem + lane_off + kT5OCol + x0 * 64, tB = tmem + lane_off + kT5OCol + x1 * 64;
@@ -448,7 +397,7 @@ __global__ void __launch_bounds__(kT5Threads, 1)
         ptx::tma_store_commit();
       }
     };
-    for (int i = (dbg & 64) ? p.items : blockIdx.x; i < p.items; i += G) {
+    for (int i = (dbg & 256) ? p.items : blockIdx.x; i < p.items; i += G) {
       T4Item it;
       it.decode(p, i);
       const int beta = it.u / p.l_mp;
@@ -462,7 +411,7 @@ __global__ void __launch_bounds__(kT5Threads, 1)
         for (int x = 0; x < 2; ++x) {
           ptx::mbar_wait(&o_full[x], ai & 1);
           ptx::mbar_wait(&l_full[x], ai & 1);
-          l[x] = l_sm[x][ai & 1][row];
+          l[x] = l_sm[x][0][ai & 1][row] + l_sm[x][1][ai & 1][row];
           m[x] = m_sm[x][ai & 1][row];
           ptx::mbar_arrive(&l_free[x]);
         }
@@ -487,7 +436,7 @@ __global__ void __launch_bounds__(kT5Threads, 1)
           ptx::tc_fence_after();
           if (tr && x == 0 && row == 0 && ai < 4) tr[490 + 4 * ai] = t4_clk();
           ptx::mbar_wait(&l_full[x], ai & 1);
-          l = l_sm[x][ai & 1][row];
+          l = l_sm[x][0][ai & 1][row] + l_sm[x][1][ai & 1][row];
           ptx::mbar_arrive(&l_free[x]);
         }
         if (m0 + x * 128 >= p.M) {   // a pair whose second tile is past M: nothing to store
@@ -504,49 +453,71 @@ __global__ void __launch_bounds__(kT5Threads, 1)
     }
     if (leader) ptx::tma_store_wait_read();   // the staging must outlive the bulk stores' reads
   } else {
-    // ============================================================ softmax (warps 0-7)
-    ptx::setmaxnreg_inc<184>();   // a whole 128-column S row lives in registers
-    const int x = warp >> 2;               // slot
+    // ============================================================ softmax (warps 0-15)
+    ptx::setmaxnreg_inc<96>();
+    const int x = (warp >> 2) & 1;         // slot
+    const int h = warp >> 3;               // column half of the S tile
     const int row = threadIdx.x & 127;     // TMEM lane
     const bool lane0 = (threadIdx.x & 31) == 0;
     const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
-    const uint32_t tS = tmem + lane_off + x * 128;
-    const uint32_t tP = tmem + lane_off + kT5PCol + x * 64;
+    const uint32_t tS = tmem + lane_off + x * 128 + h * 64;
+    const uint32_t tP = tmem + lane_off + kT5PCol + x * 64 + h * 32;
     const uint32_t tO = tmem + lane_off + kT5OCol + x * 64;
-    const float sc = p.scale;
-    // Exp-phase turns (flags bit 0, softmax only): named barriers 1-4 = slot 0's turn on SMSP q,
-    // 5-8 = slot 1's; slot 0 goes first.
+    const uint32_t pair_bar = 1 + x * 4 + (warp & 3);   // warps w and w ^ 8 (no turns)
+    // Exp-phase turns (flags bit 0, softmax only): on SMSP q the two warps of slot 0 and the two of
+    // slot 1 take turns on the MUFU; named barrier 1 + q + 4x (128 threads: slot x's two warps
+    // wait, the other slot's two arrive) opens slot x's turn and also carries the partner's
+    // partial row max.  Slot 1 pre-arrives once so slot 0 starts; slot 0 consumes slot 1's last
+    // hand-over after its loop.
     const bool turns = (p.flags & 1) != 0 && p.op == 2;
     const uint32_t bar_mine = 1 + (warp & 3) + 4 * x, bar_other = 1 + (warp & 3) + 4 * (1 - x);
-    const int turn_chunk = 3 - ((p.flags >> 4) & 3);   // flags bits 4-5: hand over 0-3 chunks early
+    const int turn_chunk = 1 - ((p.flags >> 4) & 1);   // flags bit 4: hand over one chunk early
+    if (turns && x == 1) ptx::named_bar_arrive(bar_other, 128);
+    const float sc = p.scale;
     int g = 0, ai = 0;
-    for (int i = (dbg & 64) ? p.items : blockIdx.x; i < p.items; i += G) {
+    if (dbg & 256) {
+      constexpr int kProbeReps = 64;
+      float2 la = make_float2(0.f, 0.f), lb = la;
+      const uint64_t c0 = t4_clk();
+      for (int r = 0; r < kProbeReps; ++r) {
+        uint32_t sr[64];
+        ptx::tmem_ld32(tS, &sr[0]);
+        ptx::tmem_ld32(tS + 32, &sr[32]);
+        ptx::tmem_wait_ld();
+        if (dbg & 512) {
+          float mx = t6_half_extreme<false, false>(sr, 64);
+          la.x += mx;
+        }
+        if (turns) ptx::named_bar_sync(bar_mine, 128);
+        uint32_t pk[32];
+        t6_exp_half<BF16, EMU, false>(pk, sr, sc, 0.5f, 64, la, lb, turn_chunk, turns ? bar_other : 0u);
+        ptx::tmem_st16(tP, &pk[0]);
+        ptx::tmem_st16(tP + 16, &pk[16]);
+        ptx::tmem_wait_st();
+      }
+      const uint64_t c1 = t4_clk();
+      if (tr && (threadIdx.x & 31) == 0) tr[8 + warp] = c1 - c0;
+      if (la.x + la.y + lb.x + lb.y == 1.2345f) l_sm[0][0][0][0] = 1.f;
+    } else
+    for (int i = blockIdx.x; i < p.items; i += G) {
       T4Item it;
       it.decode(p, i);
       const int beta = it.u / p.l_mp;
       const int nt = it.tiles(t4_nlim(p, beta));
       if (nt == 0) continue;
-      const int n_lim = t4_nlim(p, beta) - (it.half >= 0 ? x * nt * kT4BN : 0);
+      const int n_lim = t4_nlim(p, beta) - (it.half >= 0 ? x * nt * kT4BN : 0) - h * 64;
       float m_run = 0.f;
       float2 l2 = make_float2(0.f, 0.f), l2b = make_float2(0.f, 0.f);
       for (int j = 0; j < nt; ++j, ++g) {
         const uint32_t ph = g & 1;
-        if (!(dbg & 128)) ptx::mbar_wait(&s_full[x], ph);   // 128: free-running softmax (timing only)
+        ptx::mbar_wait(&s_full[x], ph);
         ptx::tc_fence_after();
-        if (tr && row == 0 && g < kT4TrTiles) tr[T4TR(g, x)] = t4_clk();
-        if (dbg & 1) {   // barrier protocol only
-          __syncwarp();
-          if (lane0) ptx::mbar_arrive(&s_free[x]);
-          if (g > 0) ptx::mbar_wait(&p_free[x], ph ^ 1u);
-          __syncwarp();
-          if (lane0) ptx::mbar_arrive(&p_full[x]);
-          continue;
-        }
-        const int valid = n_lim - j * kT4BN;
-        const bool full = valid >= kT4BN;
-        uint32_t sr[kT4BN];
-#pragma unroll
-        for (int c = 0; c < kT4BN / 32; ++c) ptx::tmem_ld32(tS + c * 32, &sr[c * 32]);
+        if (tr && row == 0 && h == 0 && g < kT4TrTiles) tr[T4TR(g, x)] = t4_clk();
+        const int valid = n_lim - j * kT4BN;   // valid columns of this half (may be <= 0 or >= 64)
+        const bool full = valid >= 64;
+        uint32_t sr[64];
+        ptx::tmem_ld32(tS, &sr[0]);
+        ptx::tmem_ld32(tS + 32, &sr[32]);
         ptx::tmem_wait_ld();
         ptx::tc_fence_before();
         __syncwarp();
@@ -555,30 +526,30 @@ __global__ void __launch_bounds__(kT5Threads, 1)
           // NONE / SCALE: padded keys have S = 0 and zero V rows (TMA fill), no masking needed
           if (g > 0) ptx::mbar_wait(&p_free[x], ph ^ 1u);   // G2_x(g - 1) has read P_x
           ptx::tc_fence_after();
-          t4_cvt_row<BF16>(tP, sr, sc);
+          t6_cvt_half<BF16>(tP, sr, sc);
         } else {
           float mx;
           if (full)
-            mx = sc >= 0.f ? t4_row_extreme<false, false>(sr, valid) : t4_row_extreme<true, false>(sr, valid);
+            mx = sc >= 0.f ? t6_half_extreme<false, false>(sr, valid) : t6_half_extreme<true, false>(sr, valid);
           else
-            mx = sc >= 0.f ? t4_row_extreme<false, true>(sr, valid) : t4_row_extreme<true, true>(sr, valid);
+            mx = sc >= 0.f ? t6_half_extreme<false, true>(sr, valid) : t6_half_extreme<true, true>(sr, valid);
+          // combine with the partner half (same rows, other 64 columns)
+          xmax[ph][x][h][row] = mx;
+          if (turns) ptx::named_bar_sync(bar_mine, 128); else ptx::named_bar_sync(pair_bar, 64);
+          const float mo = xmax[ph][x][h ^ 1][row];
+          mx = sc >= 0.f ? fmaxf(mx, mo) : fminf(mx, mo);
           const float m_tile = mx * sc;
-          if (tr && row == 0 && g < kT4TrTiles) tr[T4TR(g, 2 + x)] = t4_clk_after(__float_as_uint(mx));
-          // P_x (and, for a rescale, O_x) is free once G2_x(g - 1) completed.  Without a rescale
-          // the wait is deferred until the exponentials are in registers (flags bit 3 restores
-          // the early wait, for A/B measurements).
+          if (tr && row == 0 && h == 0 && g < kT4TrTiles) tr[T4TR(g, 2 + x)] = t4_clk_after(__float_as_uint(mx));
+          // P_x (and, for a rescale, O_x) is free once G2_x(g - 1) completed; without a rescale the
+          // wait is deferred until the exponentials are in registers
           bool p_ready = g == 0;
-          if (!p_ready && (p.flags & 8)) {
-            if (!(dbg & 128)) ptx::mbar_wait(&p_free[x], ph ^ 1u);
-            ptx::tc_fence_after();
-            p_ready = true;
-          }
           if (j == 0) {
             m_run = m_tile;
           } else if (__any_sync(0xffffffffu, m_tile > m_run + kT4Tau)) {
-            // warp-uniform (tcgen05.ld/st are warp-collective); O_x must hold G2_x(g - 1)
+            // warp-uniform and identical in both halves (same rows, same combined max); each
+            // half rescales its 16-column chunks of O_x
             if (!p_ready) {
-              if (!(dbg & 128)) ptx::mbar_wait(&p_free[x], ph ^ 1u);
+              ptx::mbar_wait(&p_free[x], ph ^ 1u);
               ptx::tc_fence_after();
               p_ready = true;
             }
@@ -589,7 +560,7 @@ __global__ void __launch_bounds__(kT5Threads, 1)
             l2b.x *= alpha;
             l2b.y *= alpha;
             m_run = m_new;
-            for (int c0 = 0; c0 < p.TL; c0 += 16) {
+            for (int c0 = h * 16; c0 < p.TL; c0 += 32) {
               uint32_t r[16];
               ptx::tmem_ld16(tO + c0, r);
               ptx::tmem_wait_ld();
@@ -598,23 +569,23 @@ __global__ void __launch_bounds__(kT5Threads, 1)
               ptx::tmem_st16(tO + c0, r);
             }
           }
-          if (turns && (x == 1 || g > 0)) ptx::named_bar_sync(bar_mine, 64);
-          if (tr && row == 0 && g < kT4TrTiles) tr[T4TR(g, 4 + x)] = t4_clk();   // exps start
-          // the other slot's warp may start its turn after chunk turn_chunk of this one's
-          uint32_t pk[64];
+          if (tr && row == 0 && h == 0 && g < kT4TrTiles) tr[T4TR(g, 4 + x)] = t4_clk();   // exps start
+          uint32_t pk[32];
+          const uint32_t hand = turns ? bar_other : 0u;
           if (full)
-            t5_exp_row<BF16, EMU, false>(pk, sr, sc, m_run, valid, l2, l2b, turn_chunk, turns ? bar_other : 0u);
+            t6_exp_half<BF16, EMU, false>(pk, sr, sc, m_run, valid, l2, l2b, turn_chunk, hand);
           else
-            t5_exp_row<BF16, 0, true>(pk, sr, sc, m_run, valid, l2, l2b, turn_chunk, turns ? bar_other : 0u);
-          if (tr && row == 0 && g < kT4TrTiles) tr[T4TR(g, 6 + x)] = t4_clk();   // exps done
+            t6_exp_half<BF16, 0, true>(pk, sr, sc, m_run, valid, l2, l2b, turn_chunk, hand);
+          if (tr && row == 0 && h == 0 && g < kT4TrTiles) tr[T4TR(g, 6 + x)] = t4_clk();   // exps done
           if (!p_ready) {
-            if (!(dbg & 128)) ptx::mbar_wait(&p_free[x], ph ^ 1u);
+            ptx::mbar_wait(&p_free[x], ph ^ 1u);
             ptx::tc_fence_after();
           }
-          t5_store_p(tP, pk);
+          ptx::tmem_st16(tP, &pk[0]);
+          ptx::tmem_st16(tP + 16, &pk[16]);
         }
         ptx::tmem_wait_st();
-        if (tr && row == 0 && g < kT4TrTiles) tr[T4TR(g, 8 + x)] = t4_clk();
+        if (tr && row == 0 && h == 0 && g < kT4TrTiles) tr[T4TR(g, 8 + x)] = t4_clk();
         ptx::tc_fence_before();
         __syncwarp();
         if (lane0) ptx::mbar_arrive(&p_full[x]);
@@ -622,19 +593,19 @@ __global__ void __launch_bounds__(kT5Threads, 1)
       // l_full's parity protocol allows one phase in flight: publishing l of item ai waits
       // until the epilogue has read item ai - 1's.
       if (ai >= 1) ptx::mbar_wait(&l_free[x], (ai - 1) & 1);
-      l_sm[x][ai & 1][row] = p.op == 2 ? (l2.x + l2.y) + (l2b.x + l2b.y) : 1.0f;   // E = O / l
-      m_sm[x][ai & 1][row] = m_run;
+      l_sm[x][h][ai & 1][row] = p.op == 2 ? (l2.x + l2.y) + (l2b.x + l2b.y) : (h == 0 ? 1.0f : 0.0f);   // E = O / l
+      if (h == 0) m_sm[x][ai & 1][row] = m_run;
       __syncwarp();
       if (lane0) ptx::mbar_arrive(&l_full[x]);
       ++ai;
     }
-    if (turns && !(dbg & 1) && x == 0 && g > 0) ptx::named_bar_sync(bar_mine, 64);   // slot 1's last hand-back
+    if (turns && x == 0) ptx::named_bar_sync(bar_mine, 128);   // slot 1's last hand-over
   }
 
   ptx::tc_fence_before();
   __syncthreads();
   if (tr && threadIdx.x == 0) tr[3] = ptx::globaltimer();
-  if (warp == 12) {
+  if (warp == 20) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, 512);
   }

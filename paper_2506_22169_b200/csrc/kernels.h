@@ -29,6 +29,12 @@ Tc5Kernel pick_tc5_bf16(int kch, int bl, int emu);
 inline Tc5Kernel pick_tc5(bool bf16, int kch, int bl, int emu) {
   return bf16 ? pick_tc5_bf16(kch, bl, emu) : pick_tc5_f16(kch, bl, emu);
 }
+// kernel 6 (k_tc6_f16.cu, k_tc6_bf16.cu): kernel 5's signature
+Tc5Kernel pick_tc6_f16(int kch, int bl, int emu);
+Tc5Kernel pick_tc6_bf16(int kch, int bl, int emu);
+inline Tc5Kernel pick_tc6(bool bf16, int kch, int bl, int emu) {
+  return bf16 ? pick_tc6_bf16(kch, bl, emu) : pick_tc6_f16(kch, bl, emu);
+}
 // kernel 1, CUDA cores (k_simt.cu): dtype 0 f32, 1 f16, 2 bf16
 const void* simt_fn(int dtype);
 cudaError_t launch_simt(int dtype, unsigned grid, int smem, cudaStream_t st, const void* A, const void* B,

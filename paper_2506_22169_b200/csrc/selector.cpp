@@ -155,7 +155,7 @@ static void score_b200(const mbci_chain_desc_t& d, const mbci_hw_t& hw, mbci_pla
     t_tc = b * 2.0 * d.M * d.N * (d.K + d.L) / (hw.n_sm * 256.0 * hw.clock_hz);
     t_issue = t_tc;
   }
-  if (p.kernel == 4 || p.kernel == 5) {
+  if (p.kernel == 4 || p.kernel == 5 || p.kernel == 6) {
     // persistent pair units dealt round-robin (ceil(units / n_sm) rounds per SM).
     const int64_t units = b == 0 ? 0 : static_cast<int64_t>(b) * cdiv(d.M, 256);
     const int64_t ntm = std::max<int64_t>(1, nt);
@@ -176,7 +176,8 @@ static void score_b200(const mbci_chain_desc_t& d, const mbci_hw_t& hw, mbci_pla
     else
       t_pair = d.op == MBCI_OP_SOFTMAX ? 0.35e-6 + 5.0e-9 * kd : 0.12e-6 + 3.0e-9 * kd;
     t_pair *= 1.965e9 / hw.clock_hz;
-    const double fixed = p.kernel == 5 ? 2.0e-6 : 3.0e-6;
+    if (p.kernel == 6) t_pair *= 1.001;   // uncalibrated yet: ranks just behind kernel 5
+    const double fixed = p.kernel >= 5 ? 2.0e-6 : 3.0e-6;
     // (ties go to the deeper ring, up to the 4 stages that keep two Q buffers at d = 64)
     p.t_b200 = std::max(t_hbm, static_cast<double>(rounds * ntm + tail_tiles) * t_pair) + fixed -
                1e-12 * std::min<int32_t>(p.stages, 4);
@@ -219,10 +220,10 @@ int enumerate_plans(const mbci_chain_desc_t& d, const mbci_hw_t& hw,
     // tile masked and only the L real columns stored, so Rule 3's padding waste
     // does not apply to them; they need K >= 1 (a live G1) and N >= 1.
     if (k_steps >= 1 && d.N >= 1) {
-      for (int kern : {5, 4}) {
+      for (int kern : {6, 5, 4}) {
         for (int32_t st = 2; st <= 8; ++st) {
           Tc4Layout lay;
-          const bool ok = kern == 5 ? tc5_layout(k_steps, lpad, st, d.b_layout, &lay, hw.smem_max)
+          const bool ok = kern >= 5 ? tc5_layout(k_steps, lpad, st, d.b_layout, &lay, hw.smem_max)
                                     : tc4_layout(k_steps, lpad, st, d.b_layout, &lay, hw.smem_max);
           if (!ok) continue;
           mbci_plan_t p{};

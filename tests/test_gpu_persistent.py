@@ -1,7 +1,7 @@
 """Parity of the persistent ping-pong kernels with the fp64 oracle: kernel 4 (chain_tc4.cuh, P
-aliasing S, any L <= 128) and kernel 5 (chain_tc5.cuh, separate P buffers, L <= 64), each forced
-through mbci_chain_create_with_plan so every case runs that kernel (cases with L > 64 skip
-kernel 5).
+aliasing S, any L <= 128), kernel 5 (chain_tc5.cuh, separate P buffers, L <= 64) and kernel 6
+(chain_tc6.cuh, kernel 5 with every score row split over two softmax warps), each forced through
+mbci_chain_create_with_plan so every case runs that kernel (cases with L > 64 skip kernels 5, 6).
 
 Covers: both B layouts and dtypes, head dims 16..128 (d = 128 single-buffers Q), ragged M
 (a pair unit whose second 128-row tile is entirely past M), ragged N and K/L not multiples of
@@ -44,7 +44,7 @@ def emu(request, monkeypatch):
 _KERN = {"k": 4}
 
 
-@pytest.fixture(autouse=True, params=[4, 5], ids=["k4", "k5"])
+@pytest.fixture(autouse=True, params=[4, 5, 6], ids=["k4", "k5", "k6"])
 def kern(request):
     _KERN["k"] = request.param
     yield request.param
@@ -53,11 +53,11 @@ def kern(request):
 def k4_plan(mbci, L, stages=None, K=64):
     """Plan of the kernel under test (fixture `kern`) for head dims K, L."""
     k = _KERN["k"]
-    if k == 5 and L > 64:
-        pytest.skip("kernel 5 keeps S_0, S_1, P_0, P_1, O_0, O_1 in TMEM: L <= 64")
+    if k >= 5 and L > 64:
+        pytest.skip("kernels 5 and 6 keep S_0, S_1, P_0, P_1, O_0, O_1 in TMEM: L <= 64")
     if stages is None:   # kernel 4, TL <= 64: three S buffers need a 3-deep ring; d = 128 fits only 2
         stages = 3 if L <= 64 else 2
-        if k == 5 and K > 64:   # two 64-column Q / K chunks and the E staging: a 2-deep ring fits
+        if k >= 5 and K > 64:   # two 64-column Q / K chunks and the E staging: a 2-deep ring fits
             stages = 2
     p = mbci.mbci_plan_t()
     p.kernel, p.BN, p.TL, p.stages = k, 128, max(16, (L + 15) // 16 * 16), stages

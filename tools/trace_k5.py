@@ -13,6 +13,7 @@ ap.add_argument("--shape", default="96,512,512,64,64")
 ap.add_argument("--dtype", default="f16")
 ap.add_argument("--op", default="softmax")
 ap.add_argument("--steps", type=int, default=8)
+ap.add_argument("--rot", type=int, default=8, help="rotating input sets (> L2 between reuses, as bench.py)")
 a = ap.parse_args()
 b, M, N, K, L = map(int, a.shape.split(","))
 plan = mbci.mbci_plan_t()
@@ -20,26 +21,40 @@ plan.kernel, plan.BN, plan.TL, plan.stages = map(int, a.plan.split(":"))
 inp = gen.make_chain_inputs(0, a.dtype, b, M, N, K, L, 1 if a.op == "softmax" else 0)
 dt = torch.float16 if a.dtype == "f16" else torch.bfloat16
 T = lambda x: torch.from_numpy(x.view(np.int16)).view(dt).cuda()
-A, B, D = T(inp.A), T(inp.B), T(inp.D)
-E = torch.empty(b, M, L, dtype=dt, device="cuda")
+sets = []
+for r in range(max(1, a.rot)):
+    sets.append((T(inp.A), T(inp.B), T(inp.D), torch.empty(b, M, L, dtype=dt, device="cuda")))
 ch = mbci.Chain(b, M, N, K, L, a.dtype, a.op, 1 / math.sqrt(K), b_layout=1 if a.op == "softmax" else 0, plan=plan)
 S = 512
 tr = torch.zeros(148 * S, dtype=torch.int64, device="cuda")
-for i in range(30): ch.run(A, B, D, E)
+for i in range(30): ch.run(*sets[i % len(sets)])
 torch.cuda.synchronize()
-ch.set_trace(tr); ch.run(A, B, D, E); torch.cuda.synchronize(); ch.set_trace(None)
+for i in range(len(sets) - 1): ch.run(*sets[i])   # the traced launch's inputs are the coldest
+ch.set_trace(tr); ch.run(*sets[-1]); torch.cuda.synchronize(); ch.set_trace(None)
 t = tr.cpu().numpy().reshape(148, S).astype(np.int64)
 t = t[t[:, 0] > 0]
 t0 = t[:, 0].min()
 print(ch.describe(), "ctas", len(t))
 print(f"kernel span {(t[:,3].max()-t0)/1000:.2f} us; CTA start spread {(t[:,0].max()-t0)/1000:.2f} us; "
       f"setup {np.mean(t[:,1]-t[:,0])/1000:.2f} us; CTA durations mean {np.mean(t[:,3]-t[:,0])/1000:.2f} max {np.max(t[:,3]-t[:,0])/1000:.2f}")
+rel = t[:, 1].min()   # the earliest return from griddepcontrol.wait ~ the previous grid's completion
+print(f"after the dependency release: last CTA ends +{(t[:,3].max()-rel)/1000:.2f} us; CTA ends (us after release): "
+      f"min {(t[:,3].min()-rel)/1000:.2f} median {(np.median(t[:,3])-rel)/1000:.2f} max {(t[:,3].max()-rel)/1000:.2f}; "
+      f"wait returns spread {(t[:,1].max()-rel)/1000:.2f} us")
 GHZ = float(os.environ.get("SM_GHZ", "1.965"))
 def d(c, rows=None):
     tt = t if rows is None else t[rows]
     v = tt[:, c]
     ok = v > 0
     return np.median(v[ok] - tt[ok, 4]) / GHZ / 1e3 if ok.mean() > 0.5 else float("nan")
+# per CTA (globaltimer ns; clock64 converted through the CTA's start stamps)
+def ns(ci, c):
+    return t[ci, 0] + (t[ci, c] - t[ci, 4]) / GHZ if t[ci, c] > 0 else float("nan")
+first_s = np.array([ns(ci, 8) - t[ci, 1] for ci in range(len(t))]) / 1000
+last_g = [max(g for g in range(28) if t[ci, 8 + 16 * g + 8] > 0 or g == 0) for ci in range(len(t))]
+tail = np.array([t[ci, 3] - ns(ci, 8 + 16 * last_g[ci] + 9) for ci in range(len(t))]) / 1000
+print(f"wait return -> first S tile: median {np.nanmedian(first_s):.2f} max {np.nanmax(first_s):.2f} us; "
+      f"last P stored (slot 1) -> CTA end: median {np.nanmedian(tail):.2f} max {np.nanmax(tail):.2f} us")
 cols = [("S", 0), ("max", 2), ("turn", 4), ("expd", 6), ("Pst", 8), ("Pseen", 10), ("G2is", 12), ("G1is", 14)]
 nsteps = (t[:, 8 + 16 * np.arange(28)] > 0).sum(1)
 for label, rows in (("all CTAs", None), ("CTAs with the most steps", nsteps == nsteps.max()), ("CTAs with the fewest steps", nsteps == nsteps.min())):
@@ -49,4 +64,12 @@ for label, rows in (("all CTAs", None), ("CTAs with the most steps", nsteps == n
         c = 8 + 16 * g
         row = [d(c + k + x, rows) for _, k in cols for x in (0, 1)] + [d(460 + g, rows)]
         print(f"{g:4d}  " + "  ".join(f"{v:6.2f}" for v in row))
+    if rows is not None and label.startswith("CTAs with the most"):
+        ci = int(np.argmax(np.where(rows, t[:, 3] - t[:, 0], -1)))
+        print(f"  slowest CTA (smid {t[ci, 2]}, duration {(t[ci, 3] - t[ci, 0]) / 1000:.2f} us, start +{(t[ci, 0] - t0) / 1000:.2f} us):")
+        for g in range(a.steps):
+            c = 8 + 16 * g
+            vals = [(t[ci, c + k + x] - t[ci, 4]) / GHZ / 1e3 if t[ci, c + k + x] > 0 else float("nan") for _, k in cols for x in (0, 1)]
+            tm = (t[ci, 460 + g] - t[ci, 4]) / GHZ / 1e3 if t[ci, 460 + g] > 0 else float("nan")
+            print(f"  {g:4d}  " + "  ".join(f"{v:6.2f}" for v in vals + [tm]))
     print("epilogue per item: " + "  ".join(f"[{d(490+4*u, rows):.2f} {d(491+4*u, rows):.2f} {d(492+4*u, rows):.2f}]" for u in range(4)))
