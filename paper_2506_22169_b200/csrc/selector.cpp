@@ -176,11 +176,13 @@ static void score_b200(const mbci_chain_desc_t& d, const mbci_hw_t& hw, mbci_pla
     else
       t_pair = d.op == MBCI_OP_SOFTMAX ? 0.35e-6 + 5.0e-9 * kd : 0.12e-6 + 3.0e-9 * kd;
     t_pair *= 1.965e9 / hw.clock_hz;
-    if (p.kernel == 6) t_pair *= 1.001;   // uncalibrated yet: ranks just behind kernel 5
+    // kernel 6 measures within noise of kernel 5 on softmax and slower on NONE / SCALE
+    // (round 2, profiles/r2_k5_k6_prefetch_ab.txt): it ranks just behind kernel 5
+    if (p.kernel == 6) t_pair *= 1.001;
     const double fixed = p.kernel >= 5 ? 2.0e-6 : 3.0e-6;
     // (ties go to the deeper ring, up to the 4 stages that keep two Q buffers at d = 64)
     p.t_b200 = std::max(t_hbm, static_cast<double>(rounds * ntm + tail_tiles) * t_pair) + fixed -
-               1e-12 * std::min<int32_t>(p.stages, 4);
+               1e-12 * std::min<int32_t>(p.stages, 4) + (p.kernel == 6 ? 1e-9 : 0.0);
     return;
   }
   int32_t occ = 1;

@@ -112,13 +112,13 @@ def test_enumerated_plans_are_legal_and_scored(m, shape, b_layout):
     if any(x % 8 for x in (K, b_inner, L)):        # TMA needs 16-byte row strides
         assert [p.kernel for p in plans] == [1]
         return
-    assert {p.kernel for p in plans} <= {0, 4, 5}
+    assert {p.kernel for p in plans} <= {0, 4, 5, 6}
     for p in plans:
-        assert p.kernel in (0, 4, 5) and p.BN in (64, 128)
-        assert p.BM == (256 if p.kernel in (4, 5) else 128)   # kernels 4, 5: two 128-row Q tiles per CTA
-        if p.kernel in (4, 5):    # whole L in the CTA, 128-key tiles
+        assert p.kernel in (0, 4, 5, 6) and p.BN in (64, 128)
+        assert p.BM == (256 if p.kernel >= 4 else 128)   # kernels 4-6: two 128-row Q tiles per CTA
+        if p.kernel >= 4:    # whole L in the CTA, 128-key tiles
             assert p.TL == lpad and p.BN == 128
-        if p.kernel == 5:         # S_0, S_1 + P_0, P_1 + O_0, O_1 in 512 TMEM columns
+        if p.kernel >= 5:         # S_0, S_1 + P_0, P_1 + O_0, O_1 in 512 TMEM columns
             assert p.TL <= 64
         assert p.TL % 16 == 0 and 16 <= p.TL <= lpad
         assert p.TK == max(16, math.ceil(K / 16) * 16)
@@ -145,7 +145,7 @@ def test_bert_base_prefers_full_L_tile(m):
     d = m.make_desc(96, 512, 512, 64, 64, "f16", "softmax")
     p = m.mbci_plan_t()
     assert m.mbci_plan_select(ctypes.byref(d), None, ctypes.byref(p)) == m.MBCI_OK
-    assert p.TL == 64 and p.kernel in (0, 4, 5)
+    assert p.TL == 64 and p.kernel in (0, 4, 5, 6)
 
 
 def test_fp32_and_misaligned_go_to_cuda_cores(m):
@@ -194,7 +194,7 @@ def test_persistent_plans_for_attention_shapes(m):
     d = m.make_desc(512, 4096, 4096, 128, 128, "bf16", "softmax", 0.125)
     st, plans = m.plan_enumerate(d, hw)
     assert plans[0].kernel == 4 and plans[0].stages == 2 and plans[0].TL == 128
-    assert not any(p.kernel == 5 for p in plans)
+    assert not any(p.kernel in (5, 6) for p in plans)
 
 
 @pytest.mark.parametrize("N", [192, 320, 448, 576, 960, 1000, 512])
