@@ -179,6 +179,7 @@ struct mbci_chain {
   Tc5Kernel tc5 = nullptr;   // kernels 5 / 6 (same parameter block, plus E's tensor map)
   int32_t threads = 0;       // block size of the persistent kernels
   Tc4Params tp4{};
+  Tf32Params tp7{};          // kernel 7 (fp32, 3xTF32)
   int32_t grid2 = 0;
   int32_t kch = 1, dch = 1;
   MapCacheEntry cache[16];   // tensor maps of the 16 most recent (A, B, D) pointer triples
@@ -308,6 +309,26 @@ mbci_status_t setup_plan(mbci_chain* h) {
                                                       p.smem_bytes);
     if (e != cudaSuccess) return cuda_fail(e, "occupancy query");
     if (occ < 1) return fail(MBCI_ERR_UNSUPPORTED, "kernel-%d CTA does not fit on an SM", p.kernel);
+  } else if (p.kernel == 7) {
+    if (d.dtype != MBCI_F32 || d.K < 1 || d.K > 64 || d.L > 64 || d.N < 1)
+      return fail(MBCI_ERR_UNSUPPORTED, "kernel-7 plan needs fp32, 1 <= K <= 64, L <= 64, N >= 1");
+    Tf32Params& t = h->tp7;
+    t = Tf32Params{};
+    t.M = (int32_t)d.M; t.N = (int32_t)d.N; t.K = (int32_t)d.K; t.L = (int32_t)d.L;
+    t.KP = (int32_t)((d.K + 7) / 8 * 8);
+    t.TLP = (int32_t)std::max<int64_t>(16, (d.L + 15) / 16 * 16);
+    t.op = d.op;
+    t.scale = d.op == MBCI_OP_SOFTMAX ? d.scale * 1.4426950408889634f : (d.op == MBCI_OP_SCALE ? d.scale : 1.0f);
+    t.b_layout = d.b_layout;
+    t.ld_a = d.ld_a; t.ld_b = d.ld_b; t.ld_d = d.ld_d; t.ld_e = d.ld_e;
+    t.bs_a = d.bs_a; t.bs_b = d.bs_b; t.bs_d = d.bs_d; t.bs_e = d.bs_e;
+    t.idesc1 = ptx::idesc_f16(2u, 0u, 0u, 128, 64);           // kind::tf32: a/b format 2, K-major
+    t.idesc2 = ptx::idesc_f16(2u, 0u, 0u, 128, (uint32_t)t.TLP);
+    p.n_block = d.batch * ((d.M + 127) / 128);
+    if (p.n_block > INT32_MAX) return fail(MBCI_ERR_UNSUPPORTED, "kernel-7 grid exceeds 2^31 - 1 CTAs");
+    p.smem_bytes = (int32_t)kTf32Smem;
+    cudaError_t e = cudaFuncSetAttribute(tf32_fn(), cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_bytes);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
   } else {
     if (d.batch * d.M > INT32_MAX) return fail(MBCI_ERR_UNSUPPORTED, "batch * M exceeds the CUDA-core grid");
     p.n_block = d.batch * d.M;
@@ -330,7 +351,7 @@ mbci_status_t launch(mbci_chain* h, const void* A, const void* B, const void* D,
   if (d.mask == MBCI_MASK_KEY_PADDING && !valid_len)
     return fail(MBCI_ERR_INVALID, "mask KEY_PADDING needs valid_len");
   const int32_t* vl = d.mask == MBCI_MASK_KEY_PADDING ? valid_len : nullptr;
-  if (h->plan.kernel == 0 || h->plan.kernel >= 4) {
+  if (h->plan.kernel == 0 || (h->plan.kernel >= 4 && h->plan.kernel <= 6)) {
     if (!aligned16(E) || (d.N > 0 && !aligned16(D)) || (d.K > 0 && d.N > 0 && (!aligned16(A) || !aligned16(B))))
       return fail(MBCI_ERR_UNSUPPORTED, "tensor-core path needs 16-byte aligned A, B, D, E");
     // tensor maps (cached by pointer triple)
@@ -403,6 +424,12 @@ mbci_status_t launch(mbci_chain* h, const void* A, const void* B, const void* D,
       cudaError_t le = cudaLaunchKernelEx(&cfg, h->tc5, ent->ta, ent->tb, ent->td, ent->te, t);
       if (le != cudaSuccess) return cuda_fail(le, "kernel-5/6 launch");
     }
+  } else if (h->plan.kernel == 7) {
+    Tf32Params t = h->tp7;
+    t.valid_len = vl;
+    cudaError_t le = launch_tf32((unsigned)h->plan.n_block, st, (const float*)A, (const float*)B, (const float*)D,
+                                 (float*)E, t);
+    if (le != cudaSuccess) return cuda_fail(le, "kernel-7 launch");
   } else {
     SimtParams sp{};
     sp.M = (int32_t)d.M;
@@ -574,7 +601,7 @@ mbci_status_t create_impl(const mbci_chain_desc_t* desc, int device, const mbci_
   if (forced) {
     bool found = false;
     for (const auto& p : plans)
-      if (p.kernel == forced->kernel && (p.kernel == 1 || (p.BN == forced->BN && p.TL == forced->TL &&
+      if (p.kernel == forced->kernel && (p.kernel == 1 || p.kernel == 7 || (p.BN == forced->BN && p.TL == forced->TL &&
                                                            p.stages == forced->stages))) {
         h->plan = p;
         found = true;
@@ -591,7 +618,7 @@ mbci_status_t create_impl(const mbci_chain_desc_t* desc, int device, const mbci_
     // The shortlist keeps the best-ranked plans of every kernel family so that a model error
     // between families cannot hide the fastest kernel.
     std::vector<mbci_plan_t> shortlist;
-    for (int fam : {6, 5, 4, 0, 1}) {
+    for (int fam : {7, 6, 5, 4, 0, 1}) {
       int taken = 0;
       for (const auto& q : plans)
         if (q.kernel == fam && taken < 3) {
@@ -714,14 +741,14 @@ mbci_status_t mbci_chain_describe(mbci_chain_t h, char* buf, size_t len) {
   snprintf(buf, len,
            "kernel=%s BM=%d BN=%d TK=%d TL=%d stages=%d smem=%d tmem=%d n_block=%lld "
            "t_estm=%.3gs alpha=%.4f t_b200=%.3gs",
-           p.kernel == 0 ? "tcgen05" : (p.kernel == 4 ? "tcgen05-pingpong" : (p.kernel == 5 ? "tcgen05-pingpong-sepP" : (p.kernel == 6 ? "tcgen05-pingpong-splitrow" : "simt"))), p.BM, p.BN, p.TK, p.TL, p.stages, p.smem_bytes, p.tmem_cols,
+           p.kernel == 0 ? "tcgen05" : (p.kernel == 4 ? "tcgen05-pingpong" : (p.kernel == 5 ? "tcgen05-pingpong-sepP" : (p.kernel == 6 ? "tcgen05-pingpong-splitrow" : (p.kernel == 7 ? "tcgen05-tf32x3" : "simt")))), p.BM, p.BN, p.TK, p.TL, p.stages, p.smem_bytes, p.tmem_cols,
            (long long)p.n_block, p.t_estm, p.alpha, p.t_b200);
   return MBCI_OK;
 }
 
 mbci_status_t mbci_chain_set_trace(mbci_chain_t h, void* buf, int64_t cap_bytes) {
   if (!h) return fail(MBCI_ERR_INVALID, "handle is NULL");
-  const int64_t need = h->plan.kernel >= 4 ? (int64_t)h->grid2 * kT4TraceSlots * 8
+  const int64_t need = (h->plan.kernel >= 4 && h->plan.kernel <= 6) ? (int64_t)h->grid2 * kT4TraceSlots * 8
                                              : h->plan.n_block * kTraceSlots * 8;
   if (buf && cap_bytes < need) return fail(MBCI_ERR_INVALID, "trace buffer needs %lld bytes", (long long)need);
   h->trace = static_cast<uint64_t*>(buf);

@@ -1,0 +1,15 @@
+// k_tf32.cu — kernel 7 (chain_tf32.cuh): fp32 chain on tcgen05 (kind::tf32, 3xTF32).
+#define MBCI_TF32_KERNEL 1
+#include "kernels.h"
+
+namespace mbci {
+
+const void* tf32_fn() { return (const void*)k_chain_tf32; }
+
+cudaError_t launch_tf32(unsigned grid, cudaStream_t st, const float* A, const float* B, const float* D, float* E,
+                        const Tf32Params& p) {
+  k_chain_tf32<<<grid, kTf32Threads, kTf32Smem, st>>>(A, B, D, E, p);
+  return cudaGetLastError();
+}
+
+}  // namespace mbci

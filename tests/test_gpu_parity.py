@@ -207,12 +207,18 @@ def test_strided_operands(mbci, kernel):
 
 # ------------------------------------------------------------------ fp32 + CUDA-core path
 def test_fp32_chain_C1(mbci):
-    """BASELINE config 0: fp32, batch 1, M=N=128, K=L=16, no inter-op, 1e-5."""
+    """BASELINE config 0: fp32, batch 1, M=N=128, K=L=16, no inter-op, 1e-5 — on the default plan
+    (kernel 7, tcgen05 3xTF32) and on the CUDA-core fallback (kernel 1)."""
     inp = gen.make_chain_inputs(0, "f32", 1, 128, 128, 16, 16, 0)
     err, ch = check(mbci, inp, "none", 1.0)
+    assert ch.plan().kernel == 7
+    k1 = mbci.mbci_plan_t()
+    k1.kernel = 1
+    err, ch = check(mbci, inp, "none", 1.0, plan=k1)
     assert ch.plan().kernel == 1
     inp2 = gen.make_chain_inputs(1, "f32", 2, 100, 130, 24, 20, 1)
-    check(mbci, inp2, "softmax", 0.2)
+    for plan in (None, k1):
+        check(mbci, inp2, "softmax", 0.2, plan=plan)
 
 
 def test_unaligned_16bit_uses_cuda_cores(mbci):
