@@ -8,7 +8,10 @@
  *                                  "(batch, M, N) × (batch, N, H)";  this ABI writes L for H;
  *   PAPER.md:498 (§VI-B2)          self-attention: a softmax between the two contractions;
  *   PAPER.md:253 (§III-B)          with K <= 128 the k loop is dead, A is loaded once per
- *                                  CTA and C never leaves the chip (one fused kernel).
+ *                                  CTA and C never leaves the chip (one fused kernel);
+ *   PAPER.md:426-441 (Table II)    G3-G6: H (= L) up to 256 and K up to 1024 — larger K runs a
+ *                                  live k loop (A and B streamed in 64-column chunks), larger
+ *                                  L is cut into <= 128-column h chunks bound to the grid.
  * For every batch index b (b = batch x heads):
  *   C[m,n] = sum_k A[b,m,k] * B[b,k,n]                  (fp32 accumulate)
  *   NONE:    C' = C
@@ -43,7 +46,7 @@ typedef enum { MBCI_MASK_NONE = 0, MBCI_MASK_KEY_PADDING = 1 } mbci_mask_t;
 typedef enum {
   MBCI_OK = 0,
   MBCI_ERR_INVALID = 1,      /* user error: NULL pointer, negative dim, bad enum, missing valid_len */
-  MBCI_ERR_UNSUPPORTED = 2,  /* legal but outside this build: K or L > 128, misaligned TMA strides
+  MBCI_ERR_UNSUPPORTED = 2,  /* legal but outside this build: K or L > 65536, misaligned TMA strides
                                 with no fallback, no sm_100 device */
   MBCI_ERR_CUDA = 3,         /* CUDA runtime / driver failure (detail in mbci_last_error) */
   MBCI_ERR_NOMEM = 4         /* host or device allocation failed */
@@ -102,8 +105,8 @@ typedef struct {
 
 /* Validate `desc`, pick a plan (tile selector) for `device`, and return a handle.
  * Host-only unless desc->tune == 1 (then it allocates scratch and times candidates on
- * `device`).  Errors: INVALID (NULL, negative dims, bad enums), UNSUPPORTED (K or L > 128,
- * device is not sm_100), CUDA, NOMEM. */
+ * `device`).  Errors: INVALID (NULL, negative dims, bad enums), UNSUPPORTED (K or L > 65536,
+ * no legal plan, device is not sm_100), CUDA, NOMEM. */
 mbci_status_t mbci_chain_create(const mbci_chain_desc_t* desc, int device, mbci_chain_t* out);
 
 /* As mbci_chain_create with an explicit plan (tests: plan invariance).  Fields used: kernel,

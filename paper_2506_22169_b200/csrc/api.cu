@@ -53,9 +53,9 @@ mbci_status_t normalize(const mbci_chain_desc_t* in, mbci_chain_desc_t* d) {
     return fail(MBCI_ERR_INVALID, "KEY_PADDING requires op SOFTMAX");
   if (d->b_layout != 0 && d->b_layout != 1) return fail(MBCI_ERR_INVALID, "bad b_layout %d", d->b_layout);
   if (d->tune != 0 && d->tune != 1) return fail(MBCI_ERR_INVALID, "bad tune %d", d->tune);
-  if (d->K > 128 || d->L > 128)
-    return fail(MBCI_ERR_UNSUPPORTED, "K=%lld L=%lld: this build fuses K, L <= 128 only",
-                (long long)d->K, (long long)d->L);
+  if (d->K > kMaxK || d->L > kMaxL)
+    return fail(MBCI_ERR_UNSUPPORTED, "K=%lld L=%lld: this build takes K, L <= %lld",
+                (long long)d->K, (long long)d->L, (long long)kMaxK);
   const int64_t b_inner = d->b_layout == 0 ? d->N : d->K;
   const int64_t b_rows = d->b_layout == 0 ? d->K : d->N;
   if (d->ld_a == 0) d->ld_a = d->K;
@@ -204,7 +204,8 @@ mbci_status_t setup_plan(mbci_chain* h) {
     p.smem_bytes = static_cast<int32_t>(
         tc_smem_bytes(k_steps, p.BN, p.TL, p.stages, d.b_layout, &a_bytes, &b_stage, &d_stage));
     p.tmem_cols = tmem_alloc_cols(p.BN, p.TL);
-    h->kch = std::max(1, (16 * k_steps + 63) / 64);
+    const bool stream = k_steps > 8;   // K > 128: live k loop (chain_tc.cuh, TcParams::kc)
+    h->kch = stream ? 1 : std::max(1, (16 * k_steps + 63) / 64);
     h->dch = (p.TL + 63) / 64;
     h->tc = pick_tc(d.dtype == MBCI_BF16, p.BN, h->kch, d.b_layout, h->dch);
     TcParams& t = h->tp;
@@ -225,7 +226,8 @@ mbci_status_t setup_plan(mbci_chain* h) {
     t.a_bytes = (uint32_t)a_bytes;
     t.b_stage_bytes = (uint32_t)b_stage;
     t.d_stage_bytes = (uint32_t)d_stage;
-    t.kp_rows = (uint32_t)(16 * k_steps);
+    t.kp_rows = (uint32_t)(stream ? 64 : 16 * k_steps);
+    t.kc = stream ? (int32_t)((d.K + 63) / 64) : 0;
     t.tmem_cols = (uint32_t)p.tmem_cols;
     const uint32_t fmt = d.dtype == MBCI_BF16 ? 1u : 0u;
     t.idesc1 = ptx::idesc_f16(fmt, 0, d.b_layout == 0 ? 1u : 0u, 128, (uint32_t)p.BN);
@@ -373,7 +375,7 @@ mbci_status_t launch(mbci_chain* h, const void* A, const void* B, const void* D,
       if (d.K > 0 && d.N > 0) {
         s = encode3d(&ent->ta, A, bf16, d.K, d.M, d.batch, d.ld_a, d.bs_a, 128);
         if (s != MBCI_OK) return s;
-        const uint32_t kp_rows = (uint32_t)(16 * ((d.K + 15) / 16));
+        const uint32_t kp_rows = h->plan.kernel == 0 ? h->tp.kp_rows : (uint32_t)(16 * ((d.K + 15) / 16));
         if (d.b_layout == 1)
           s = encode3d(&ent->tb, B, bf16, d.K, d.N, d.batch, d.ld_b, d.bs_b, bn_box);
         else

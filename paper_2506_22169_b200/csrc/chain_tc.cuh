@@ -42,7 +42,10 @@ struct TcParams {
   uint32_t a_bytes;        // A tile bytes in SMEM (= TMA transaction bytes)
   uint32_t b_stage_bytes;  // one B stage
   uint32_t d_stage_bytes;  // one D stage
-  uint32_t kp_rows;        // B (layout 0) box rows = 16 * k_steps
+  uint32_t kp_rows;        // B (layout 0) box rows = 16 * k_steps (64 when A is streamed)
+  int32_t kc;              // 0: A resident (K <= 128); else K > 128 streamed in kc chunks of 64 columns:
+                           // ring entry (j, c) = [A[:, 64c:64c+64] | B_j[64c:64c+64]] (live k loop,
+                           // PAPER.md:230-233 with L_A in k scope)
   uint32_t tmem_cols;
   uint32_t idesc1, idesc2;
   uint64_t* trace;   // optional per-CTA event timestamps (debug; see mbci_chain_set_trace)
@@ -136,7 +139,26 @@ __global__ void __launch_bounds__(kThreads, BN == 64 ? 2 : 1)
 
   if (warp == 4) {
     // ------------------------------------------------------------ TMA producer: A, B_j
-    if (ptx::elect_one() && nt > 0 && p.k_steps > 0) {
+    const bool elected = ptx::elect_one();   // one elect.sync per warp (all 32 lanes take part)
+    if (elected && nt > 0 && p.k_steps > 0 && p.kc > 0) {
+      // live k loop: (A chunk, B chunk) pairs, A re-read from L2 for every key tile
+      for (int j = 0, e = 0; j < nt; ++j) {
+        for (int c = 0; c < p.kc; ++c, ++e) {
+          const int s = e % S;
+          if (e >= S) ptx::mbar_wait(&b_empty[s], ((e / S) - 1) & 1);
+          uint8_t* dst = sB + s * p.b_stage_bytes;
+          ptx::mbar_arrive_expect_tx(&b_full[s], p.b_stage_bytes);
+          ptx::tma_load_3d(dst, &tmA, &b_full[s], c * 64, m0, beta);
+          if constexpr (BL == 1) {
+            ptx::tma_load_3d(dst + 16384, &tmB, &b_full[s], c * 64, j * BN, beta);
+          } else {
+#pragma unroll
+            for (int nb = 0; nb < BN / 64; ++nb)
+              ptx::tma_load_3d(dst + 16384 + nb * (64 * 128), &tmB, &b_full[s], j * BN + nb * 64, c * 64, beta);
+          }
+        }
+      }
+    } else if (elected && nt > 0 && p.k_steps > 0) {
       ptx::mbar_arrive_expect_tx(a_full, p.a_bytes);
 #pragma unroll
       for (int c = 0; c < KCH; ++c) ptx::tma_load_3d(sA + c * 16384, &tmA, a_full, c * 64, m0, beta);
@@ -173,11 +195,32 @@ __global__ void __launch_bounds__(kThreads, BN == 64 ? 2 : 1)
     // ------------------------------------------------------------ tcgen05 issuer
     if (ptx::elect_one() && nt > 0) {
       const uint32_t tO = tmem + 2 * BN;
-      if (p.k_steps > 0) ptx::mbar_wait(a_full, 0);
+      if (p.k_steps > 0 && p.kc == 0) ptx::mbar_wait(a_full, 0);
       if (tr) tr[kTrAFull] = ptx::globaltimer();
       const uint32_t a_base = ptx::smem_u32(sA);
       for (int j = 0; j <= nt; ++j) {
-        if (j < nt) {
+        if (j < nt && p.kc > 0) {   // live k loop: S_j = sum over chunks c of A_c · B_j,c
+          const int buf = j & 1;
+          for (int c = 0; c < p.kc; ++c) {
+            const int e = j * p.kc + c, s = e % S;
+            ptx::mbar_wait(&b_full[s], (e / S) & 1);
+            ptx::tc_fence_after();
+            const uint32_t e_base = ptx::smem_u32(sB + s * p.b_stage_bytes);
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) {
+              const uint64_t ad = ptx::sdesc_sw128(e_base + ks * 32, 16, 1024);
+              uint64_t bd;
+              if constexpr (BL == 1)
+                bd = ptx::sdesc_sw128(e_base + 16384 + ks * 32, 16, 1024);
+              else
+                bd = ptx::sdesc_sw128(e_base + 16384 + ks * 2048, 64 * 128, 1024);
+              ptx::mma_ss(tmem + buf * BN, ad, bd, p.idesc1, (c > 0 || ks > 0) ? 1u : 0u);
+            }
+            ptx::mma_commit(&b_empty[s]);
+          }
+          if (tr && j < kTrTiles) tr[MBCI_TR(j, 5)] = ptx::globaltimer();
+          ptx::mma_commit(&s_full[buf]);
+        } else if (j < nt) {
           const int s = j % S, buf = j & 1;
           if (p.k_steps > 0) {
             ptx::mbar_wait(&b_full[s], (j / S) & 1);

@@ -67,8 +67,11 @@ int64_t tc_smem_bytes(int32_t k_steps, int32_t BN, int32_t TL, int32_t stages, i
   const int32_t kp = 16 * k_steps;
   const int32_t kch = std::max<int32_t>(1, static_cast<int32_t>(cdiv(kp, 64)));
   const int32_t dch = static_cast<int32_t>(cdiv(TL, 64));
-  const int32_t a = k_steps > 0 ? kch * 16384 : 0;
-  const int32_t b = k_steps == 0 ? 0 : (b_layout == 1 ? kch * BN * 128 : (BN / 64) * kp * 128);
+  const bool stream = k_steps > 8;   // K > 128: live k loop, ring entry = A chunk + B chunk (64 columns)
+  const int32_t a = (k_steps > 0 && !stream) ? kch * 16384 : 0;
+  const int32_t b = k_steps == 0 ? 0
+                    : stream     ? 16384 + BN * 128
+                                 : (b_layout == 1 ? kch * BN * 128 : (BN / 64) * kp * 128);
   const int32_t d = dch * BN * 128;
   if (a_bytes) *a_bytes = a;
   if (b_stage) *b_stage = b;
@@ -122,7 +125,7 @@ int32_t tmem_alloc_cols(int32_t BN, int32_t TL) {
 
 bool tc_eligible(const mbci_chain_desc_t& d) {
   if (d.dtype != MBCI_F16 && d.dtype != MBCI_BF16) return false;
-  if (d.K > 128 || d.L > 128) return false;
+  if (d.K > kMaxK || d.L > kMaxL) return false;
   // TMA: every row / batch stride a multiple of 16 bytes (8 elements)
   const int64_t strides[8] = {d.ld_a, d.ld_b, d.ld_d, d.ld_e, d.bs_a, d.bs_b, d.bs_d, d.bs_e};
   for (int64_t v : strides)
@@ -221,7 +224,7 @@ int enumerate_plans(const mbci_chain_desc_t& d, const mbci_hw_t& hw,
     // Persistent families (kernels 5 and 4): one 128-key tile per step with the ragged last
     // tile masked and only the L real columns stored, so Rule 3's padding waste
     // does not apply to them; they need K >= 1 (a live G1) and N >= 1.
-    if (k_steps >= 1 && d.N >= 1) {
+    if (k_steps >= 1 && k_steps <= 8 && d.N >= 1) {   // K <= 128: Q tiles resident (dead k loop)
       for (int kern : {6, 5, 4}) {
         for (int32_t st = 2; st <= 8; ++st) {
           Tc4Layout lay;
@@ -249,7 +252,7 @@ int enumerate_plans(const mbci_chain_desc_t& d, const mbci_hw_t& hw,
       const bool apply_rule3 = rule3 && (pass == 0);
       for (int32_t BN : {64, 128}) {
         if (apply_rule3 && d.N > 0 && rule3_reject(d.N, BN)) continue;
-        for (int32_t TL = 16; TL <= lpad; TL += 16) {
+        for (int32_t TL = 16; TL <= std::min<int32_t>(lpad, 128); TL += 16) {   // L > 128: h chunks on the grid
           if (apply_rule3 && d.L > 0 && rule3_reject(d.L, TL)) continue;
           if (2 * BN + TL > hw.tmem_cols) continue;  // TMEM budget
           for (int32_t st = 2; st <= 4; ++st) {

@@ -7,6 +7,11 @@
 
 namespace mbci {
 
+// Largest reduction dims the ABI accepts (K: live k loop in 64-column chunks on kernel 0;
+// L: h chunks of <= 128 columns on the grid, PAPER.md:230-233 / Table II G3-G6).
+constexpr int64_t kMaxK = 65536;
+constexpr int64_t kMaxL = 65536;
+
 void model_terms(int64_t batch, int64_t M, int64_t N, int64_t K, int64_t L, int64_t TM,
                  int64_t TN, int64_t TK, int64_t TH, int32_t s, const mbci_hw_t& hw,
                  double out[5]);

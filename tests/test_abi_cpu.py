@@ -60,8 +60,8 @@ def test_validation_errors(m):
     assert _create(m, d)[0] == m.MBCI_ERR_INVALID
     d = m.make_desc(1, 8, 8, 8, 8, op="none", mask=True)
     assert _create(m, d)[0] == m.MBCI_ERR_INVALID
-    assert _create(m, m.make_desc(1, 8, 8, 129, 8))[0] == m.MBCI_ERR_UNSUPPORTED
-    assert _create(m, m.make_desc(1, 8, 8, 64, 256))[0] == m.MBCI_ERR_UNSUPPORTED
+    assert _create(m, m.make_desc(1, 8, 8, 65537, 8))[0] == m.MBCI_ERR_UNSUPPORTED    # K, L <= 65536
+    assert _create(m, m.make_desc(1, 8, 8, 64, 65537))[0] == m.MBCI_ERR_UNSUPPORTED
     d = m.make_desc(1, 8, 8, 16, 8, strides={"ld_a": 8})   # row stride shorter than the row
     assert _create(m, d)[0] == m.MBCI_ERR_INVALID
     assert b"stride" in m.mbci_last_error()
@@ -218,3 +218,22 @@ def test_persistent_kernel_default_on_any_N(m, N):
     assert st == m.MBCI_OK and plans[0].kernel == 4
     st, plans = m.plan_enumerate(m.make_desc(4, 256, N, 128, 128, "bf16", "softmax", 0.125))
     assert {4, 0} <= {p.kernel for p in plans}     # a candidate even where kernel 0 ranks first
+
+
+@pytest.mark.parametrize("K,L", [(256, 256), (512, 256), (1024, 256), (64, 256), (136, 64), (4096, 136)])
+def test_large_K_L_plans_are_kernel0_with_live_k_loop_or_h_chunks(m, K, L):
+    """SURVEY §8(f) f3 (Table II G3-G6): K > 128 streams A and B in 64-column chunks
+    (ring entry = 16 KB A chunk + BN x 128 B B chunk, no resident A), L > 128 is cut into h chunks
+    of TL <= 128 columns; only kernel 0 takes these shapes, and every plan fits SMEM and TMEM."""
+    hw = m.mbci_hw_t()
+    m.mbci_hw_default(ctypes.byref(hw))
+    st, plans = m.plan_enumerate(m.make_desc(1, 512, 512, K, L, "f16", "none", 1.0, b_layout=0), hw)
+    assert st == m.MBCI_OK and plans and all(p.kernel == 0 for p in plans)
+    for p in plans:
+        assert p.TL <= 128 and p.TL % 16 == 0 and p.smem_bytes <= hw.smem_max
+        assert 2 * p.BN + p.TL <= 512
+        if K > 128:   # no resident A: stages x (A chunk + B chunk) + stages x D stage + barriers
+            dch = (p.TL + 63) // 64
+            assert p.smem_bytes >= p.stages * (16384 + p.BN * 128 + dch * p.BN * 128)
+    fp32 = m.plan_enumerate(m.make_desc(1, 512, 512, K, L, "f32", "none", 1.0))[1]
+    assert [p.kernel for p in fp32] == ([7, 1] if K <= 64 and L <= 64 else [1])
