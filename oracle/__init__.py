@@ -54,6 +54,10 @@ def lib():
                                    ctypes.c_int, ctypes.c_double, ctypes.c_int, vp, vp, i64,
                                    ctypes.c_int, dp]
         L.oracle_chain.restype = ctypes.c_int
+        L.oracle_chain_ex.argtypes = [vp, vp, vp, dp, ctypes.c_int, i64, i64, i64, i64, i64,
+                                      ctypes.c_int, ctypes.c_double, ctypes.c_int, vp, ctypes.c_int, vp, i64,
+                                      ctypes.c_int, dp]
+        L.oracle_chain_ex.restype = ctypes.c_int
         L.oracle_decode_array.argtypes = [vp, ctypes.c_int, i64, dp]
         L.oracle_decode_array.restype = ctypes.c_int
         L.oracle_max_threads.restype = ctypes.c_int
@@ -84,11 +88,12 @@ def decode(bits: np.ndarray, dtype: str) -> np.ndarray:
 
 
 def chain(inp, op: str, scale: float = 1.0, valid_len=None, rows=None,
-          nthreads: int = 0, want_cprime: bool = False):
+          nthreads: int = 0, want_cprime: bool = False, causal: bool = False):
     """fp64 E for ``inp`` (an ``mbci_inputs.ChainInputs``).
 
     rows: None (all rows; E is [batch, M, L]) or an int64 array of (β, m) pairs
     (E is [len(rows), L]).  valid_len: None or int32[batch] (softmax key padding).
+    causal: softmax sees key n from row m only if n <= m (R18).
     Returns E, or (E, C') when want_cprime.
     """
     A = np.ascontiguousarray(inp.A)
@@ -104,10 +109,10 @@ def chain(inp, op: str, scale: float = 1.0, valid_len=None, rows=None,
         nrows = rr.shape[0]
         E = np.empty((nrows, inp.L), dtype=np.float64)
     Cp = np.empty((nrows, inp.N), dtype=np.float64) if want_cprime else None
-    rc = lib().oracle_chain(_ptr(A), _ptr(B), _ptr(D), _ptr(E), DTYPE_CODE[inp.dtype],
-                            inp.batch, inp.M, inp.N, inp.K, inp.L, OP_CODE[op], float(scale),
-                            inp.b_layout, _ptr(vl), _ptr(rr), 0 if rr is None else nrows,
-                            int(nthreads), _ptr(Cp))
+    rc = lib().oracle_chain_ex(_ptr(A), _ptr(B), _ptr(D), _ptr(E), DTYPE_CODE[inp.dtype],
+                               inp.batch, inp.M, inp.N, inp.K, inp.L, OP_CODE[op], float(scale),
+                               inp.b_layout, _ptr(vl), 1 if causal else 0, _ptr(rr),
+                               0 if rr is None else nrows, int(nthreads), _ptr(Cp))
     if rc != 0:
         raise ValueError("oracle_chain rejected its arguments")
     return (E, Cp) if want_cprime else E

@@ -23,7 +23,9 @@
  *   2. C[n] = sum_{k<K} A[β,m,k] * B[β,k,n]            (B per b_layout)
  *   3. op:  NONE  C'[n] = C[n]
  *           SCALE C'[n] = s*C[n]
- *           SOFTMAX z[n] = s*C[n] (or -inf if n >= valid_len[β]);
+ *           SOFTMAX z[n] = s*C[n] (or -inf if n >= valid_len[β], or, with the causal
+ *                   mask, if n > m — top-left aligned as torch SDPA is_causal; R18,
+ *                   SURVEY §8(f) f4 / PAPER.md:194 "more ... operators");
  *                   mu = max_n z[n]; if mu == -inf: C'[n] = 0 for all n;
  *                   else e[n] = exp(z[n]-mu), Z = sum_n e[n], C'[n] = e[n]/Z
  *   4. E[β,m,l] = sum_{n<N} C'[n] * D[β,n,l]
@@ -141,10 +143,30 @@ static int64_t clamp_vlen(int op, const int32_t* valid_len, int64_t beta, int64_
  * SOFTMAX; values clamp to [0, N]).  Cprime: NULL or double[rows, N].
  * Returns 0, or -1 on invalid arguments / allocation failure.
  */
+/* the key limit of row m: valid_len (clamped) and, with the causal mask, keys n <= m only */
+static int64_t row_limit(int64_t vlen, int causal, int64_t m) {
+  return (causal && m + 1 < vlen) ? m + 1 : vlen;
+}
+
+int oracle_chain_ex(const void* A, const void* B, const void* D, double* E, int dtype,
+                    int64_t batch, int64_t M, int64_t N, int64_t K, int64_t L, int op,
+                    double scale, int b_layout, const int32_t* valid_len, int causal,
+                    const int64_t* rows, int64_t nrows, int nthreads, double* Cprime);
+
 int oracle_chain(const void* A, const void* B, const void* D, double* E, int dtype,
                  int64_t batch, int64_t M, int64_t N, int64_t K, int64_t L, int op,
                  double scale, int b_layout, const int32_t* valid_len,
                  const int64_t* rows, int64_t nrows, int nthreads, double* Cprime) {
+  return oracle_chain_ex(A, B, D, E, dtype, batch, M, N, K, L, op, scale, b_layout, valid_len, 0, rows,
+                         nrows, nthreads, Cprime);
+}
+
+/* As oracle_chain; causal != 0 adds the causal mask to SOFTMAX (key n visible to row m iff n <= m). */
+int oracle_chain_ex(const void* A, const void* B, const void* D, double* E, int dtype,
+                    int64_t batch, int64_t M, int64_t N, int64_t K, int64_t L, int op,
+                    double scale, int b_layout, const int32_t* valid_len, int causal,
+                    const int64_t* rows, int64_t nrows, int nthreads, double* Cprime) {
+  if (op != ORC_OP_SOFTMAX) causal = 0;
   if (batch < 0 || M < 0 || N < 0 || K < 0 || L < 0 || nrows < 0) return -1;
   if (dtype < 0 || dtype > 2 || op < 0 || op > 2 || b_layout < 0 || b_layout > 1) return -1;
 #ifdef _OPENMP
@@ -170,7 +192,7 @@ int oracle_chain(const void* A, const void* B, const void* D, double* E, int dty
         decode_span(D, dtype, beta * N * L, N * L, d);
         int64_t vlen = clamp_vlen(op, valid_len, beta, N);
         for (int64_t m = 0; m < M; ++m)
-          chain_row(a + m * K, b, d, N, K, L, op, scale, b_layout, vlen, C,
+          chain_row(a + m * K, b, d, N, K, L, op, scale, b_layout, row_limit(vlen, causal, m), C,
                     E + (beta * M + m) * L, Cprime ? Cprime + (beta * M + m) * N : NULL);
       }
       free(a); free(b); free(d); free(C);
@@ -191,8 +213,9 @@ int oracle_chain(const void* A, const void* B, const void* D, double* E, int dty
         decode_span(A, dtype, (beta * M + m) * K, K, a);
         decode_span(B, dtype, beta * K * N, K * N, b);
         decode_span(D, dtype, beta * N * L, N * L, d);
-        chain_row(a, b, d, N, K, L, op, scale, b_layout, clamp_vlen(op, valid_len, beta, N),
-                  C, E + r * L, Cprime ? Cprime + r * N : NULL);
+        chain_row(a, b, d, N, K, L, op, scale, b_layout,
+                  row_limit(clamp_vlen(op, valid_len, beta, N), causal, m), C, E + r * L,
+                  Cprime ? Cprime + r * N : NULL);
       }
       free(a); free(b); free(d); free(C);
     }

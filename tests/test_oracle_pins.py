@@ -127,6 +127,43 @@ def test_softmax_key_padding_matches_torch_sdpa():
     assert np.max(np.abs(ours - ref)) < 1e-12
 
 
+@pytest.mark.parametrize("M,N", [(40, 40), (33, 90), (90, 33)])
+def test_causal_matches_torch_sdpa(M, N):
+    """Causal mask (R18: key n visible to row m iff n <= m, top-left aligned) against
+    torch SDPA's is_causal (tril(diagonal=0) of an M x N ones matrix) in fp64, square and not."""
+    inp = gen.make_chain_inputs(23, "f16", 3, M, N, 64, 32, 1)
+    A, B, D = _f64(inp)
+    ours = oracle.chain(inp, "softmax", 0.125, causal=True)
+    ref = torch.nn.functional.scaled_dot_product_attention(
+        torch.from_numpy(A), torch.from_numpy(B), torch.from_numpy(D), is_causal=True, scale=0.125).numpy()
+    assert np.max(np.abs(ours - ref)) < 1e-12
+
+
+def test_causal_closed_forms_and_padding():
+    """Row 0 sees key 0 only (E = D[0,:] exactly); D = ones gives E = 1; with key padding the
+    limit is min(valid_len, m + 1) — a fully padded batch row stays 0; NONE ignores the flag."""
+    inp = gen.make_chain_inputs(24, "bf16", 3, 50, 60, 16, 8, 1)
+    E = oracle.chain(inp, "softmax", 0.5, causal=True)
+    D = gen.bits_to_f64_numpy(inp.D, "bf16")
+    assert np.array_equal(E[:, 0, :], D[:, 0, :])
+    ones = gen.ChainInputs(inp.A, inp.B, np.full(inp.D.shape, 0x3F80, dtype=np.uint16), None, "bf16", 3, 50, 60,
+                           16, 8, 1)
+    assert np.max(np.abs(oracle.chain(ones, "softmax", 0.5, causal=True) - 1.0)) < 1e-12
+    vl = np.array([60, 10, 0], dtype=np.int32)
+    Ec = oracle.chain(inp, "softmax", 0.5, valid_len=vl, causal=True)
+    A, B, _ = _f64(inp)
+    for b, v in enumerate(vl):
+        for m in (0, 5, 9, 10, 30, 49):
+            lim = min(v, m + 1)
+            if lim == 0:
+                assert np.all(Ec[b, m] == 0.0)
+                continue
+            z = 0.5 * (A[b, m] @ B[b, :lim].T)
+            p = np.exp(z - z.max())
+            assert np.max(np.abs(Ec[b, m] - (p / p.sum()) @ D[b, :lim])) < 1e-12
+    assert np.array_equal(oracle.chain(inp, "none", 1.0, causal=True), oracle.chain(inp, "none", 1.0))
+
+
 @pytest.mark.parametrize("b_layout", [0, 1])
 def test_identity_D_exposes_op(b_layout):
     """D = I (L = N)  =>  E = op(A·B): numpy matmul and scipy softmax as references."""
