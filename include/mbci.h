@@ -42,7 +42,15 @@ typedef struct mbci_chain* mbci_chain_t;   /* opaque; created/owned by the libra
 
 typedef enum { MBCI_F32 = 0, MBCI_F16 = 1, MBCI_BF16 = 2 } mbci_dtype_t;
 typedef enum { MBCI_OP_NONE = 0, MBCI_OP_SCALE = 1, MBCI_OP_SOFTMAX = 2 } mbci_op_t;
-typedef enum { MBCI_MASK_NONE = 0, MBCI_MASK_KEY_PADDING = 1 } mbci_mask_t;
+/* Masks (bit flags, SOFTMAX only).  KEY_PADDING: keys n >= valid_len[b] get -inf.  CAUSAL: key n
+ * is visible to query row m only if n <= m (top-left aligned, as torch SDPA is_causal; DESIGN.md
+ * R18).  CAUSAL_KEY_PADDING: both (row limit min(valid_len[b], m + 1)). */
+typedef enum {
+  MBCI_MASK_NONE = 0,
+  MBCI_MASK_KEY_PADDING = 1,
+  MBCI_MASK_CAUSAL = 2,
+  MBCI_MASK_CAUSAL_KEY_PADDING = 3
+} mbci_mask_t;
 typedef enum {
   MBCI_OK = 0,
   MBCI_ERR_INVALID = 1,      /* user error: NULL pointer, negative dim, bad enum, missing valid_len */
@@ -65,7 +73,7 @@ typedef struct {
   int32_t dtype;        /* mbci_dtype_t */
   int32_t op;           /* mbci_op_t */
   float scale;          /* SCALE / SOFTMAX multiplier; NaN selects 1/sqrt(K) (DESIGN R1) */
-  int32_t mask;         /* mbci_mask_t; KEY_PADDING only with SOFTMAX */
+  int32_t mask;         /* mbci_mask_t; any mask only with SOFTMAX */
   int32_t b_layout;     /* 0 or 1, see above */
   int64_t ld_a, ld_b, ld_d, ld_e;
   int64_t bs_a, bs_b, bs_d, bs_e;

@@ -47,10 +47,10 @@ mbci_status_t normalize(const mbci_chain_desc_t* in, mbci_chain_desc_t* d) {
     return fail(MBCI_ERR_INVALID, "negative dimension");
   if (d->dtype < MBCI_F32 || d->dtype > MBCI_BF16) return fail(MBCI_ERR_INVALID, "bad dtype %d", d->dtype);
   if (d->op < MBCI_OP_NONE || d->op > MBCI_OP_SOFTMAX) return fail(MBCI_ERR_INVALID, "bad op %d", d->op);
-  if (d->mask != MBCI_MASK_NONE && d->mask != MBCI_MASK_KEY_PADDING)
+  if (d->mask < MBCI_MASK_NONE || d->mask > MBCI_MASK_CAUSAL_KEY_PADDING)
     return fail(MBCI_ERR_INVALID, "bad mask %d", d->mask);
-  if (d->mask == MBCI_MASK_KEY_PADDING && d->op != MBCI_OP_SOFTMAX)
-    return fail(MBCI_ERR_INVALID, "KEY_PADDING requires op SOFTMAX");
+  if (d->mask != MBCI_MASK_NONE && d->op != MBCI_OP_SOFTMAX)
+    return fail(MBCI_ERR_INVALID, "masks require op SOFTMAX");
   if (d->b_layout != 0 && d->b_layout != 1) return fail(MBCI_ERR_INVALID, "bad b_layout %d", d->b_layout);
   if (d->tune != 0 && d->tune != 1) return fail(MBCI_ERR_INVALID, "bad tune %d", d->tune);
   if (d->K > kMaxK || d->L > kMaxL)
@@ -220,6 +220,7 @@ mbci_status_t setup_plan(mbci_chain* h) {
     t.k_steps = k_steps;
     t.stages = p.stages;
     t.op = d.op;
+    t.causal = (d.mask & MBCI_MASK_CAUSAL) ? 1 : 0;
     t.scale = d.op == MBCI_OP_SOFTMAX ? d.scale * 1.4426950408889634f : d.scale;
     t.ld_e = d.ld_e;
     t.bs_e = d.bs_e;
@@ -270,6 +271,7 @@ mbci_status_t setup_plan(mbci_chain* h) {
     t.stages = p.stages;
     t.q_bufs = lay.q_bufs;
     t.op = d.op;
+    t.causal = (d.mask & MBCI_MASK_CAUSAL) ? 1 : 0;
     t.scale = d.op == MBCI_OP_SOFTMAX ? d.scale * 1.4426950408889634f : (d.op == MBCI_OP_SCALE ? d.scale : 1.0f);
     t.ld_e = d.ld_e;
     t.bs_e = d.bs_e;
@@ -320,6 +322,7 @@ mbci_status_t setup_plan(mbci_chain* h) {
     t.KP = (int32_t)((d.K + 7) / 8 * 8);
     t.TLP = (int32_t)std::max<int64_t>(16, (d.L + 15) / 16 * 16);
     t.op = d.op;
+    t.causal = (d.mask & MBCI_MASK_CAUSAL) ? 1 : 0;
     t.scale = d.op == MBCI_OP_SOFTMAX ? d.scale * 1.4426950408889634f : (d.op == MBCI_OP_SCALE ? d.scale : 1.0f);
     t.b_layout = d.b_layout;
     t.ld_a = d.ld_a; t.ld_b = d.ld_b; t.ld_d = d.ld_d; t.ld_e = d.ld_e;
@@ -350,9 +353,9 @@ mbci_status_t launch(mbci_chain* h, const void* A, const void* B, const void* D,
   if (!E) return fail(MBCI_ERR_INVALID, "E is NULL");
   if (d.N > 0 && d.L > 0 && !D) return fail(MBCI_ERR_INVALID, "D is NULL");
   if (d.K > 0 && d.N > 0 && (!A || !B)) return fail(MBCI_ERR_INVALID, "A or B is NULL");
-  if (d.mask == MBCI_MASK_KEY_PADDING && !valid_len)
+  if ((d.mask & MBCI_MASK_KEY_PADDING) && !valid_len)
     return fail(MBCI_ERR_INVALID, "mask KEY_PADDING needs valid_len");
-  const int32_t* vl = d.mask == MBCI_MASK_KEY_PADDING ? valid_len : nullptr;
+  const int32_t* vl = (d.mask & MBCI_MASK_KEY_PADDING) ? valid_len : nullptr;
   if (h->plan.kernel == 0 || (h->plan.kernel >= 4 && h->plan.kernel <= 6)) {
     if (!aligned16(E) || (d.N > 0 && !aligned16(D)) || (d.K > 0 && d.N > 0 && (!aligned16(A) || !aligned16(B))))
       return fail(MBCI_ERR_UNSUPPORTED, "tensor-core path needs 16-byte aligned A, B, D, E");
@@ -439,6 +442,7 @@ mbci_status_t launch(mbci_chain* h, const void* A, const void* B, const void* D,
     sp.K = (int32_t)d.K;
     sp.L = (int32_t)d.L;
     sp.op = d.op;
+    sp.causal = (d.mask & MBCI_MASK_CAUSAL) ? 1 : 0;
     sp.scale = d.scale;
     sp.b_layout = d.b_layout;
     sp.valid_len = vl;
@@ -698,7 +702,7 @@ mbci_status_t mbci_chain_run_host(mbci_chain_t h, const void* A, const void* B, 
   if (nB && (e = cudaMemcpyAsync(h->dB, B, nB, cudaMemcpyHostToDevice, st)) != cudaSuccess) return cuda_fail(e, "H2D B");
   if (nD && (e = cudaMemcpyAsync(h->dD, D, nD, cudaMemcpyHostToDevice, st)) != cudaSuccess) return cuda_fail(e, "H2D D");
   const int32_t* dv = nullptr;
-  if (d.mask == MBCI_MASK_KEY_PADDING) {
+  if (d.mask & MBCI_MASK_KEY_PADDING) {
     if (!valid_len) return fail(MBCI_ERR_INVALID, "mask KEY_PADDING needs valid_len");
     if ((e = cudaMemcpyAsync(h->dV, valid_len, d.batch * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess)
       return cuda_fail(e, "H2D valid_len");

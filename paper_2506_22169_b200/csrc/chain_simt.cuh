@@ -14,6 +14,7 @@ namespace mbci {
 struct SimtParams {
   int32_t M, N, K, L;
   int32_t op;
+  int32_t causal;   // softmax: key n visible to row m only if n <= m (R18)
   float scale;
   int32_t b_layout;
   const int32_t* valid_len;
@@ -68,6 +69,7 @@ __global__ void __launch_bounds__(kSimtThreads)
   const T* d = D + beta * p.bs_d;
   int vlen = p.N;
   if (p.op == 2 && p.valid_len != nullptr) vlen = min(max(p.valid_len[beta], 0), p.N);
+  if (p.op == 2 && p.causal) vlen = min(vlen, m + 1);   // key n visible to row m iff n <= m
 
   for (int n = threadIdx.x; n < p.N; n += blockDim.x) {
     float acc = 0.f;

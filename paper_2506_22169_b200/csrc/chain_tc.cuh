@@ -35,6 +35,7 @@ struct TcParams {
   int32_t k_steps;   // ceil(K / 16); 0 => C = 0
   int32_t stages;
   int32_t op;        // 0 none, 1 scale, 2 softmax
+  int32_t causal;    // softmax: key n visible to row m only if n <= m (R18)
   float scale;       // SCALE multiplier, or softmax scale * log2(e)
   const int32_t* valid_len;
   void* E;
@@ -105,6 +106,9 @@ __global__ void __launch_bounds__(kThreads, BN == 64 ? 2 : 1)
 
   int n_lim = p.N;
   if (p.op == 2 && p.valid_len != nullptr) n_lim = min(max(p.valid_len[beta], 0), p.N);
+  // causal (R18): row m sees keys n <= m; the CTA's tiles end at its last row's limit
+  const int row_lim = (p.op == 2 && p.causal) ? min(n_lim, m0 + static_cast<int>(threadIdx.x) + 1) : n_lim;
+  if (p.op == 2 && p.causal) n_lim = min(n_lim, m0 + 128);
   const int nt = (n_lim + BN - 1) / BN;
 
   if (threadIdx.x == kRowThreads) {
@@ -290,7 +294,7 @@ __global__ void __launch_bounds__(kThreads, BN == 64 ? 2 : 1)
       if (trj) tr[MBCI_TR(j, 1)] = ptx::globaltimer_after(sr[BN - 1]);
       uint32_t pk[BN / 2];
       if (p.op == 2) {
-        const int valid = n_lim - j * BN;  // >= BN for a full tile
+        const int valid = row_lim - j * BN;  // >= BN for a full tile (this thread's row)
         const bool full = valid >= BN;
         // tile max of z = sc * S over valid keys (sc >= 0: max S; sc < 0: min S)
         float mx;
@@ -373,6 +377,10 @@ __global__ void __launch_bounds__(kThreads, BN == 64 ? 2 : 1)
 #pragma unroll
       for (int c = 0; c < BN / 64; ++c) ptx::tmem_st32(tS + buf * BN + c * 32, &pk[c * 32]);
       ptx::tmem_wait_st();
+      // consume o_done's phase for G2(j - 1) every tile (it completes once per G2; the rescale
+      // above may already have waited on it): no phase goes unobserved, so parity waits stay
+      // unambiguous and compute-sanitizer --tool synccheck finds no missing wait
+      if (j >= 1) ptx::mbar_wait(o_done, (j - 1) & 1);
       ptx::tc_fence_before();
       ptx::mbar_arrive(&p_full[buf]);
       if (trj) tr[MBCI_TR(j, 4)] = ptx::globaltimer();

@@ -57,6 +57,7 @@ struct Tc4Params {
   int32_t stages;          // K/V ring depth
   int32_t q_bufs;          // Q-pair buffers (1 or 2)
   int32_t op;              // 2 softmax; 1 scale, 0 none (P = cvt(scale * S), E = O)
+  int32_t causal;          // softmax: key n visible to row m only if n <= m (R18)
   float scale;             // softmax: scale * log2(e); SCALE: the multiplier; NONE: 1
   const int32_t* valid_len;
   void* E;
@@ -104,6 +105,16 @@ __device__ __forceinline__ uint64_t t4_clk_after(uint32_t dep) {
 __device__ __forceinline__ int t4_nlim(const Tc4Params& p, int beta) {
   int n = p.N;
   if (p.valid_len != nullptr) n = min(max(__ldg(p.valid_len + beta), 0), p.N);
+  return n;
+}
+
+// Key limit of pair unit u for its tile count: key padding and, with the causal mask (DESIGN.md
+// R18), the pair's last row m0 + 255 sees keys < m0 + 256 (slot 0's rows see one tile less; that
+// tile is fully masked for them).
+__device__ __forceinline__ int t4_unit_nlim(const Tc4Params& p, int u) {
+  const int beta = u / p.l_mp;
+  int n = t4_nlim(p, beta);
+  if (p.causal) n = min(n, (u - beta * p.l_mp) * 256 + 256);
   return n;
 }
 
@@ -246,7 +257,7 @@ struct T4Cursor {
     while (i < p.items) {
       T4Item it;
       it.decode(p, i);
-      nt = it.tiles(t4_nlim(p, it.u / p.l_mp));
+      nt = it.tiles(t4_unit_nlim(p, it.u));
       if (nt > 0) {
         u = it.u;
         hf = it.half >= 0;
@@ -393,7 +404,7 @@ __global__ void __launch_bounds__(kT4Threads, 1)
         it.decode(p, i);
         const int beta = it.u / p.l_mp;
         const int m0 = (it.u - beta * p.l_mp) * 256 + (it.half > 0 ? 128 : 0);
-        const int nt = it.tiles(t4_nlim(p, beta));
+        const int nt = it.tiles(t4_unit_nlim(p, it.u));
         if (nt == 0) continue;
         load_q(0, m0, beta, it.half < 0 && m0 + 128 < p.M);
         const int per = it.half >= 0 ? 2 : 1;
@@ -422,7 +433,7 @@ __global__ void __launch_bounds__(kT4Threads, 1)
           it.decode(p, i);
           const int beta = it.u / p.l_mp;
           const int m0 = (it.u - beta * p.l_mp) * 256 + (it.half > 0 ? 128 : 0);
-          const int nt = it.tiles(t4_nlim(p, beta));
+          const int nt = it.tiles(t4_unit_nlim(p, it.u));
           if (nt == 0) continue;
           const int qb = ai % p.q_bufs;
           if (ai >= p.q_bufs) ptx::mbar_wait(&q_empty[qb], ((ai / p.q_bufs) - 1) & 1);
@@ -586,7 +597,7 @@ __global__ void __launch_bounds__(kT4Threads, 1)
       it.decode(p, i);
       const int beta = it.u / p.l_mp;
       const int m0 = (it.u - beta * p.l_mp) * 256;
-      const int nt = it.tiles(t4_nlim(p, beta));
+      const int nt = it.tiles(t4_unit_nlim(p, it.u));
       if (it.half >= 0) {
         // half item: both slots hold partial (O, m, l) of the same 128 rows (keys split between
         // them); merge by log-sum-exp, exact in real arithmetic (online-softmax identity)
@@ -682,10 +693,11 @@ __global__ void __launch_bounds__(kT4Threads, 1)
       T4Item it;
       it.decode(p, i);
       const int beta = it.u / p.l_mp;
-      const int nt = it.tiles(t4_nlim(p, beta));
+      const int nt = it.tiles(t4_unit_nlim(p, it.u));
       if (nt == 0) continue;
       // keys from this slot's first tile on (a half item's slot 1 starts at tile nt)
       const int n_lim = t4_nlim(p, beta) - (it.half >= 0 ? x * nt * kT4BN : 0);
+      const int m_row = (it.u - beta * p.l_mp) * 256 + x * 128 + row;   // causal: no half items
       float m_run = 0.f;
       float2 l2 = make_float2(0.f, 0.f), l2b = make_float2(0.f, 0.f);
       for (int j = 0; j < nt; ++j, ++g) {
@@ -699,8 +711,8 @@ __global__ void __launch_bounds__(kT4Threads, 1)
           ptx::mbar_arrive(&p_full[b]);
           continue;
         }
-        const int valid = n_lim - j * kT4BN;
-        const bool full = valid >= kT4BN;
+        const int valid = (p.causal ? min(n_lim, m_row + 1) : n_lim) - j * kT4BN;   // this thread's row
+        const bool full = __all_sync(0xffffffffu, valid >= kT4BN);                   // warp-uniform
         uint32_t sr[kT4BN];
 #pragma unroll
         for (int c = 0; c < kT4BN / 32; ++c) ptx::tmem_ld32(tS + c * 32, &sr[c * 32]);

@@ -247,7 +247,7 @@ __global__ void __launch_bounds__(kT5Threads, 1)
       it.decode(p, i);
       const int beta = it.u / p.l_mp;
       const int m0 = (it.u - beta * p.l_mp) * 256 + (it.half > 0 ? 128 : 0);
-      const int nt = it.tiles(t4_nlim(p, beta));
+      const int nt = it.tiles(t4_unit_nlim(p, it.u));
       if (nt == 0) continue;
       load_q(0, m0, beta, it.half < 0 && m0 + 128 < p.M);
       const int per = it.half >= 0 ? 2 : 1;
@@ -283,7 +283,7 @@ __global__ void __launch_bounds__(kT5Threads, 1)
           it.decode(p, i);
           const int beta = it.u / p.l_mp;
           const int m0 = (it.u - beta * p.l_mp) * 256 + (it.half > 0 ? 128 : 0);
-          const int nt = it.tiles(t4_nlim(p, beta));
+          const int nt = it.tiles(t4_unit_nlim(p, it.u));
           if (nt == 0) continue;
           const int qb = ai % p.q_bufs;
           if (ai >= p.q_bufs) wait1(&q_empty[qb], ((ai / p.q_bufs) - 1) & 1);
@@ -453,7 +453,7 @@ __global__ void __launch_bounds__(kT5Threads, 1)
       it.decode(p, i);
       const int beta = it.u / p.l_mp;
       const int m0 = (it.u - beta * p.l_mp) * 256;
-      const int nt = it.tiles(t4_nlim(p, beta));
+      const int nt = it.tiles(t4_unit_nlim(p, it.u));
       if (it.half >= 0) {
         // half item: both slots hold partial (O, m, l) of the same 128 rows; merge by
         // log-sum-exp (exact in real arithmetic, R4)
@@ -524,9 +524,10 @@ __global__ void __launch_bounds__(kT5Threads, 1)
       T4Item it;
       it.decode(p, i);
       const int beta = it.u / p.l_mp;
-      const int nt = it.tiles(t4_nlim(p, beta));
+      const int nt = it.tiles(t4_unit_nlim(p, it.u));
       if (nt == 0) continue;
       const int n_lim = t4_nlim(p, beta) - (it.half >= 0 ? x * nt * kT4BN : 0);
+      const int m_row = (it.u - beta * p.l_mp) * 256 + x * 128 + row;   // causal: no half items
       float m_run = 0.f;
       float2 l2 = make_float2(0.f, 0.f), l2b = make_float2(0.f, 0.f);
       for (int j = 0; j < nt; ++j, ++g) {
@@ -542,8 +543,8 @@ __global__ void __launch_bounds__(kT5Threads, 1)
           if (lane0) ptx::mbar_arrive(&p_full[x]);
           continue;
         }
-        const int valid = n_lim - j * kT4BN;
-        const bool full = valid >= kT4BN;
+        const int valid = (p.causal ? min(n_lim, m_row + 1) : n_lim) - j * kT4BN;   // this thread's row
+        const bool full = __all_sync(0xffffffffu, valid >= kT4BN);                   // warp-uniform
         uint32_t sr[kT4BN];
 #pragma unroll
         for (int c = 0; c < kT4BN / 32; ++c) ptx::tmem_ld32(tS + c * 32, &sr[c * 32]);

@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(kT6Threads, 1)
       it.decode(p, i);
       const int beta = it.u / p.l_mp;
       const int m0 = (it.u - beta * p.l_mp) * 256 + (it.half > 0 ? 128 : 0);
-      const int nt = it.tiles(t4_nlim(p, beta));
+      const int nt = it.tiles(t4_unit_nlim(p, it.u));
       if (nt == 0) continue;
       load_q(0, m0, beta, it.half < 0 && m0 + 128 < p.M);
       const int per = it.half >= 0 ? 2 : 1;
@@ -252,7 +252,7 @@ __global__ void __launch_bounds__(kT6Threads, 1)
           it.decode(p, i);
           const int beta = it.u / p.l_mp;
           const int m0 = (it.u - beta * p.l_mp) * 256 + (it.half > 0 ? 128 : 0);
-          const int nt = it.tiles(t4_nlim(p, beta));
+          const int nt = it.tiles(t4_unit_nlim(p, it.u));
           if (nt == 0) continue;
           const int qb = ai % p.q_bufs;
           if (ai >= p.q_bufs) wait1(&q_empty[qb], ((ai / p.q_bufs) - 1) & 1);
@@ -402,7 +402,7 @@ __global__ void __launch_bounds__(kT6Threads, 1)
       it.decode(p, i);
       const int beta = it.u / p.l_mp;
       const int m0 = (it.u - beta * p.l_mp) * 256;
-      const int nt = it.tiles(t4_nlim(p, beta));
+      const int nt = it.tiles(t4_unit_nlim(p, it.u));
       if (it.half >= 0) {
         // half item: both slots hold partial (O, m, l) of the same 128 rows; merge by
         // log-sum-exp (exact in real arithmetic, R4)
@@ -503,7 +503,7 @@ __global__ void __launch_bounds__(kT6Threads, 1)
       T4Item it;
       it.decode(p, i);
       const int beta = it.u / p.l_mp;
-      const int nt = it.tiles(t4_nlim(p, beta));
+      const int nt = it.tiles(t4_unit_nlim(p, it.u));
       if (nt == 0) continue;
       const int n_lim = t4_nlim(p, beta) - (it.half >= 0 ? x * nt * kT4BN : 0) - h * 64;
       float m_run = 0.f;

@@ -33,6 +33,7 @@ struct Tf32Params {
   int32_t KP;    // K padded to a multiple of 8 (the TF32 MMA K step), <= 64
   int32_t TLP;   // L padded to a multiple of 16 (the MMA N granularity), <= 64
   int32_t op;    // 0 none, 1 scale, 2 softmax
+  int32_t causal; // softmax: key n visible to row m only if n <= m (R18)
   float scale;   // softmax: scale * log2(e); SCALE: the multiplier
   int32_t b_layout;
   const int32_t* valid_len;
@@ -161,7 +162,10 @@ __global__ void __launch_bounds__(kTf32Threads, 1)
                  dBlo = ptx::sdesc_sw128(ptx::smem_u32(sBlo), 16, 1024),
                  dDhi = ptx::sdesc_sw128(ptx::smem_u32(sDhi), 16, 1024),
                  dDlo = ptx::sdesc_sw128(ptx::smem_u32(sDlo), 16, 1024);
-  const int ntiles = p.op == 2 ? (n_lim + kTf32BN - 1) / kTf32BN : (p.N + kTf32BN - 1) / kTf32BN;
+  // causal: the CTA's last row m0 + 127 sees keys < m0 + 128; row `row` sees keys <= m0 + row
+  const int cta_lim = (p.op == 2 && p.causal) ? min(n_lim, m0 + 128) : n_lim;
+  const int row_lim = (p.op == 2 && p.causal) ? min(n_lim, m0 + row + 1) : n_lim;
+  const int ntiles = p.op == 2 ? (cta_lim + kTf32BN - 1) / kTf32BN : (p.N + kTf32BN - 1) / kTf32BN;
   float m_run = -INFINITY, l_run = 0.f;
   // O accumulates in fp32 registers across key tiles (IEEE adds): the tensor core sums only one
   // tile's 24 products per element into TMEM (acc = 0 at each tile's first MMA), which keeps its
@@ -207,7 +211,7 @@ __global__ void __launch_bounds__(kTf32Threads, 1)
     ptx::tmem_wait_ld();
     float pv[kTf32BN];
     if (p.op == 2) {
-      const int valid = n_lim - n0;
+      const int valid = row_lim - n0;
       float mx = -INFINITY;
 #pragma unroll
       for (int c = 0; c < kTf32BN; ++c)

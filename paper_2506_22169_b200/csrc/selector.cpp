@@ -226,6 +226,7 @@ int enumerate_plans(const mbci_chain_desc_t& d, const mbci_hw_t& hw,
     // does not apply to them; they need K >= 1 (a live G1) and N >= 1.
     if (k_steps >= 1 && k_steps <= 8 && d.N >= 1) {   // K <= 128: Q tiles resident (dead k loop)
       for (int kern : {6, 5, 4}) {
+        if (kern == 6 && (d.mask & MBCI_MASK_CAUSAL)) continue;   // kernel 6 has no causal rows
         for (int32_t st = 2; st <= 8; ++st) {
           Tc4Layout lay;
           const bool ok = kern >= 5 ? tc5_layout(k_steps, lpad, st, d.b_layout, &lay, hw.smem_max)

@@ -22,7 +22,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 
 MBCI_F32, MBCI_F16, MBCI_BF16 = 0, 1, 2
 MBCI_OP_NONE, MBCI_OP_SCALE, MBCI_OP_SOFTMAX = 0, 1, 2
-MBCI_MASK_NONE, MBCI_MASK_KEY_PADDING = 0, 1
+MBCI_MASK_NONE, MBCI_MASK_KEY_PADDING, MBCI_MASK_CAUSAL, MBCI_MASK_CAUSAL_KEY_PADDING = 0, 1, 2, 3
 MBCI_OK, MBCI_ERR_INVALID, MBCI_ERR_UNSUPPORTED, MBCI_ERR_CUDA, MBCI_ERR_NOMEM = 0, 1, 2, 3, 4
 
 DTYPES = {"f32": MBCI_F32, "f16": MBCI_F16, "bf16": MBCI_BF16}
@@ -124,13 +124,13 @@ def check(status, where="mbci"):
 
 
 def make_desc(batch, M, N, K, L, dtype="bf16", op="softmax", scale=float("nan"), mask=False,
-              b_layout=1, strides=None, tune=0) -> mbci_chain_desc_t:
+              b_layout=1, strides=None, tune=0, causal=False) -> mbci_chain_desc_t:
     d = mbci_chain_desc_t()
     d.batch, d.M, d.N, d.K, d.L = batch, M, N, K, L
     d.dtype = DTYPES[dtype] if isinstance(dtype, str) else int(dtype)
     d.op = OPS[op] if isinstance(op, str) else int(op)
     d.scale = scale
-    d.mask = MBCI_MASK_KEY_PADDING if mask else MBCI_MASK_NONE
+    d.mask = (MBCI_MASK_KEY_PADDING if mask else MBCI_MASK_NONE) | (MBCI_MASK_CAUSAL if causal else 0)
     d.b_layout = b_layout
     if strides:
         for k, v in strides.items():
@@ -174,8 +174,8 @@ class Chain:
     """Handle wrapper: create once per shape, run many times (torch tensors on the device)."""
 
     def __init__(self, batch, M, N, K, L, dtype="bf16", op="softmax", scale=float("nan"), mask=False,
-                 b_layout=1, device=0, strides=None, tune=0, plan=None):
-        self.desc = make_desc(batch, M, N, K, L, dtype, op, scale, mask, b_layout, strides, tune)
+                 b_layout=1, device=0, strides=None, tune=0, plan=None, causal=False):
+        self.desc = make_desc(batch, M, N, K, L, dtype, op, scale, mask, b_layout, strides, tune, causal)
         self.device = device
         h = _vp()
         if plan is None:

@@ -27,11 +27,12 @@ def e_f64(E, dtype):
     return gen.bits_to_f64_numpy(e_bits(E), dtype)
 
 
-def run_chain(mbci, inp, op, scale, valid_len=None, plan=None, E=None, tune=0):
+def run_chain(mbci, inp, op, scale, valid_len=None, plan=None, E=None, tune=0, causal=False):
     """Create a handle for inp's shape, run once, return (E tensor, Chain)."""
     dev = torch.device("cuda", 0)
     ch = mbci.Chain(inp.batch, inp.M, inp.N, inp.K, inp.L, inp.dtype, op, scale,
-                    mask=valid_len is not None, b_layout=inp.b_layout, device=0, plan=plan, tune=tune)
+                    mask=valid_len is not None, b_layout=inp.b_layout, device=0, plan=plan, tune=tune,
+                    causal=causal)
     A = to_dev(inp.A, inp.dtype)
     B = to_dev(inp.B, inp.dtype)
     D = to_dev(inp.D, inp.dtype)
