@@ -34,7 +34,7 @@ _LIB_PATH = os.path.join(_HERE, "liboracle.so")
 _LIB = None
 
 DTYPE_CODE = {"f32": 0, "f16": 1, "bf16": 2}
-OP_CODE = {"none": 0, "scale": 1, "softmax": 2}
+OP_CODE = {"none": 0, "scale": 1, "softmax": 2, "relu": 3, "gelu": 4}
 
 
 def build(force: bool = False) -> str:

@@ -23,6 +23,8 @@
  *   2. C[n] = sum_{k<K} A[β,m,k] * B[β,k,n]            (B per b_layout)
  *   3. op:  NONE  C'[n] = C[n]
  *           SCALE C'[n] = s*C[n]
+ *           RELU  C'[n] = max(s*C[n], 0)              (R19: elementwise inter-ops,
+ *           GELU  C'[n] = g(s*C[n]), g(x) = x/2 (1 + erf(x/sqrt 2))   PAPER.md:194)
  *           SOFTMAX z[n] = s*C[n] (or -inf if n >= valid_len[β], or, with the causal
  *                   mask, if n > m — top-left aligned as torch SDPA is_causal; R18,
  *                   SURVEY §8(f) f4 / PAPER.md:194 "more ... operators");
@@ -39,7 +41,7 @@
 #endif
 
 enum { ORC_F32 = 0, ORC_F16 = 1, ORC_BF16 = 2 };
-enum { ORC_OP_NONE = 0, ORC_OP_SCALE = 1, ORC_OP_SOFTMAX = 2 };
+enum { ORC_OP_NONE = 0, ORC_OP_SCALE = 1, ORC_OP_SOFTMAX = 2, ORC_OP_RELU = 3, ORC_OP_GELU = 4 };
 
 /* IEEE 754 binary16: 1 sign, 5 exponent (bias 15), 10 fraction bits. */
 double oracle_decode_f16(uint16_t h) {
@@ -100,6 +102,10 @@ static void chain_row(const double* a, const double* b, const double* d,
   /* step 3: op */
   if (op == ORC_OP_SCALE) {
     for (int64_t n = 0; n < N; ++n) C[n] = s * C[n];
+  } else if (op == ORC_OP_RELU) {
+    for (int64_t n = 0; n < N; ++n) C[n] = (s * C[n] > 0.0) ? s * C[n] : 0.0;
+  } else if (op == ORC_OP_GELU) {
+    for (int64_t n = 0; n < N; ++n) C[n] = 0.5 * (s * C[n]) * (1.0 + erf((s * C[n]) / sqrt(2.0)));
   } else if (op == ORC_OP_SOFTMAX) {
     double mu = -INFINITY;
     for (int64_t n = 0; n < N; ++n) {
@@ -168,7 +174,7 @@ int oracle_chain_ex(const void* A, const void* B, const void* D, double* E, int 
                     const int64_t* rows, int64_t nrows, int nthreads, double* Cprime) {
   if (op != ORC_OP_SOFTMAX) causal = 0;
   if (batch < 0 || M < 0 || N < 0 || K < 0 || L < 0 || nrows < 0) return -1;
-  if (dtype < 0 || dtype > 2 || op < 0 || op > 2 || b_layout < 0 || b_layout > 1) return -1;
+  if (dtype < 0 || dtype > 2 || op < 0 || op > 4 || b_layout < 0 || b_layout > 1) return -1;
 #ifdef _OPENMP
   if (nthreads > 0) omp_set_num_threads(nthreads);
 #else

@@ -165,6 +165,27 @@ def test_causal_closed_forms_and_padding():
 
 
 @pytest.mark.parametrize("b_layout", [0, 1])
+def test_activation_ops_through_identity_D(b_layout):
+    """RELU / GELU inter-ops (R19): D = I exposes op(s·A·B) — RELU against numpy
+    maximum, GELU against scipy.special.erf's definition; GELU(x) − GELU(−x) = x exactly in real
+    arithmetic (checked through A → −A); GELU(0) = 0 (scale 0)."""
+    from scipy.special import erf as sp_erf
+    inp = gen.make_chain_inputs(35, "bf16", 2, 17, 24, 20, 24, b_layout)
+    A = gen.bits_to_f64_numpy(inp.A, "bf16")
+    B = gen.bits_to_f64_numpy(inp.B, "bf16")
+    eye = np.broadcast_to(np.eye(24), (2, 24, 24))
+    inp = _custom("bf16", A, B, eye, b_layout)
+    C = A @ (B if b_layout == 0 else np.swapaxes(B, 1, 2))
+    s = 0.7
+    assert np.max(np.abs(oracle.chain(inp, "relu", s) - np.maximum(s * C, 0.0))) < 1e-12
+    g = 0.5 * s * C * (1.0 + sp_erf(s * C / math.sqrt(2.0)))
+    assert np.max(np.abs(oracle.chain(inp, "gelu", s) - g)) < 1e-12
+    neg = _custom("bf16", -A, B, eye, b_layout)
+    assert np.max(np.abs(oracle.chain(inp, "gelu", s) - oracle.chain(neg, "gelu", s) - s * C)) < 1e-12
+    assert np.all(oracle.chain(inp, "gelu", 0.0) == 0.0)
+
+
+@pytest.mark.parametrize("b_layout", [0, 1])
 def test_identity_D_exposes_op(b_layout):
     """D = I (L = N)  =>  E = op(A·B): numpy matmul and scipy softmax as references."""
     inp = gen.make_chain_inputs(31, "bf16", 2, 17, 24, 20, 24, b_layout)
