@@ -16,6 +16,7 @@
  *   C[m,n] = sum_k A[b,m,k] * B[b,k,n]                  (fp32 accumulate)
  *   NONE:    C' = C
  *   SCALE:   C' = scale * C
+ *   RELU / GELU: C' = act(scale * C)  (elementwise, R19)
  *   SOFTMAX: C'[m,:] = softmax_n(scale * C[m,:] + mask), mask = -inf for keys
  *            n >= valid_len[b] (KEY_PADDING); a row with no valid key gives E = 0
  *   E[b,m,l] = sum_n C'[m,n] * D[b,n,l]                 (fp32 accumulate, stored as dtype)
@@ -41,7 +42,16 @@ extern "C" {
 typedef struct mbci_chain* mbci_chain_t;   /* opaque; created/owned by the library */
 
 typedef enum { MBCI_F32 = 0, MBCI_F16 = 1, MBCI_BF16 = 2 } mbci_dtype_t;
-typedef enum { MBCI_OP_NONE = 0, MBCI_OP_SCALE = 1, MBCI_OP_SOFTMAX = 2 } mbci_op_t;
+/* Inter-GEMM op on C = A·B: NONE C, SCALE s·C, SOFTMAX softmax_n(s·C + mask), and the elementwise
+ * activations RELU max(s·C, 0), GELU g(s·C) with g(x) = x/2 (1 + erf(x / sqrt 2)) (the MLP-style
+ * chain; R19). */
+typedef enum {
+  MBCI_OP_NONE = 0,
+  MBCI_OP_SCALE = 1,
+  MBCI_OP_SOFTMAX = 2,
+  MBCI_OP_RELU = 3,
+  MBCI_OP_GELU = 4
+} mbci_op_t;
 /* Masks (bit flags, SOFTMAX only).  KEY_PADDING: keys n >= valid_len[b] get -inf.  CAUSAL: key n
  * is visible to query row m only if n <= m (top-left aligned, as torch SDPA is_causal; DESIGN.md
  * R18).  CAUSAL_KEY_PADDING: both (row limit min(valid_len[b], m + 1)). */

@@ -46,7 +46,7 @@ mbci_status_t normalize(const mbci_chain_desc_t* in, mbci_chain_desc_t* d) {
   if (d->batch < 0 || d->M < 0 || d->N < 0 || d->K < 0 || d->L < 0)
     return fail(MBCI_ERR_INVALID, "negative dimension");
   if (d->dtype < MBCI_F32 || d->dtype > MBCI_BF16) return fail(MBCI_ERR_INVALID, "bad dtype %d", d->dtype);
-  if (d->op < MBCI_OP_NONE || d->op > MBCI_OP_SOFTMAX) return fail(MBCI_ERR_INVALID, "bad op %d", d->op);
+  if (d->op < MBCI_OP_NONE || d->op > MBCI_OP_GELU) return fail(MBCI_ERR_INVALID, "bad op %d", d->op);
   if (d->mask < MBCI_MASK_NONE || d->mask > MBCI_MASK_CAUSAL_KEY_PADDING)
     return fail(MBCI_ERR_INVALID, "bad mask %d", d->mask);
   if (d->mask != MBCI_MASK_NONE && d->op != MBCI_OP_SOFTMAX)
@@ -73,7 +73,9 @@ mbci_status_t normalize(const mbci_chain_desc_t* in, mbci_chain_desc_t* d) {
     return fail(MBCI_ERR_INVALID, "negative stride");
   if (d->M > INT32_MAX || d->N > INT32_MAX || d->batch > INT32_MAX)
     return fail(MBCI_ERR_UNSUPPORTED, "dimension exceeds int32");
-  if (std::isnan(d->scale)) d->scale = d->K > 0 ? 1.0f / std::sqrt(static_cast<float>(d->K)) : 1.0f;
+  if (std::isnan(d->scale))   // DESIGN.md R1 (scale, softmax) and R19 (activations: 1)
+    d->scale = (d->op == MBCI_OP_RELU || d->op == MBCI_OP_GELU || d->K == 0) ? 1.0f
+                                                                                : 1.0f / std::sqrt(static_cast<float>(d->K));
   return MBCI_OK;
 }
 
@@ -272,7 +274,7 @@ mbci_status_t setup_plan(mbci_chain* h) {
     t.q_bufs = lay.q_bufs;
     t.op = d.op;
     t.causal = (d.mask & MBCI_MASK_CAUSAL) ? 1 : 0;
-    t.scale = d.op == MBCI_OP_SOFTMAX ? d.scale * 1.4426950408889634f : (d.op == MBCI_OP_SCALE ? d.scale : 1.0f);
+    t.scale = d.op == MBCI_OP_SOFTMAX ? d.scale * 1.4426950408889634f : (d.op == MBCI_OP_NONE ? 1.0f : d.scale);
     t.ld_e = d.ld_e;
     t.bs_e = d.bs_e;
 #if MBCI_TRACE
@@ -323,7 +325,7 @@ mbci_status_t setup_plan(mbci_chain* h) {
     t.TLP = (int32_t)std::max<int64_t>(16, (d.L + 15) / 16 * 16);
     t.op = d.op;
     t.causal = (d.mask & MBCI_MASK_CAUSAL) ? 1 : 0;
-    t.scale = d.op == MBCI_OP_SOFTMAX ? d.scale * 1.4426950408889634f : (d.op == MBCI_OP_SCALE ? d.scale : 1.0f);
+    t.scale = d.op == MBCI_OP_SOFTMAX ? d.scale * 1.4426950408889634f : (d.op == MBCI_OP_NONE ? 1.0f : d.scale);
     t.b_layout = d.b_layout;
     t.ld_a = d.ld_a; t.ld_b = d.ld_b; t.ld_d = d.ld_d; t.ld_e = d.ld_e;
     t.bs_a = d.bs_a; t.bs_b = d.bs_b; t.bs_d = d.bs_d; t.bs_e = d.bs_e;

@@ -42,6 +42,12 @@ __device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float v) { return
 
 constexpr int kSimtThreads = 128;
 
+// RELU / GELU (exact erf) of x = scale * C (R19)
+__device__ __forceinline__ float act_op(int op, float x) {
+  if (op == 3) return fmaxf(x, 0.0f);
+  return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f));
+}
+
 __device__ __forceinline__ float block_reduce(float v, bool is_max, float* scratch) {
   for (int o = 16; o > 0; o >>= 1) {
     float w = __shfl_xor_sync(0xffffffffu, v, o);
@@ -78,7 +84,7 @@ __global__ void __launch_bounds__(kSimtThreads)
                                        : to_f(b[static_cast<int64_t>(n) * p.ld_b + k]);
       acc = fmaf(to_f(a[k]), bv, acc);
     }
-    c_row[n] = (p.op == 0) ? acc : p.scale * acc;
+    c_row[n] = (p.op == 0) ? acc : (p.op >= 3 ? act_op(p.op, p.scale * acc) : p.scale * acc);
   }
   __syncthreads();
   if (p.op == 2) {

@@ -370,6 +370,10 @@ __global__ void __launch_bounds__(kThreads, BN == 64 ? 2 : 1)
       } else if (p.op == 1) {
 #pragma unroll
         for (int c = 0; c < BN / 2; ++c) pk[c] = ptx::pack2<BF16>(s[2 * c] * sc, s[2 * c + 1] * sc);
+      } else if (p.op >= 3) {   // RELU / GELU of scale * S
+#pragma unroll
+        for (int c = 0; c < BN / 2; ++c)
+          pk[c] = ptx::pack2<BF16>(ptx::act(p.op, s[2 * c] * sc), ptx::act(p.op, s[2 * c + 1] * sc));
       } else {
 #pragma unroll
         for (int c = 0; c < BN / 2; ++c) pk[c] = ptx::pack2<BF16>(s[2 * c], s[2 * c + 1]);

@@ -229,8 +229,9 @@ __device__ __forceinline__ void t4_exp_row(uint32_t tS, const uint32_t (&sr)[kT4
 
 // NONE / SCALE: P = cvt(scale * S) for the 128 scores of the row, written as 16-bit P into TMEM
 // columns [0, 64) of the S buffer (no max, no exponentials, no row sum).
+// RELU / GELU (op 3 / 4): P = cvt(act(scale * S)).
 template <bool BF16>
-__device__ __forceinline__ void t4_cvt_row(uint32_t tS, const uint32_t (&sr)[kT4BN], float sc) {
+__device__ __forceinline__ void t4_cvt_row(uint32_t tS, const uint32_t (&sr)[kT4BN], float sc, int op) {
   const float2 sc2 = make_float2(sc, sc);
 #pragma unroll
   for (int ch = 0; ch < 4; ++ch) {
@@ -238,7 +239,11 @@ __device__ __forceinline__ void t4_cvt_row(uint32_t tS, const uint32_t (&sr)[kT4
 #pragma unroll
     for (int c = 0; c < 16; ++c) {
       const int cp = ch * 16 + c;
-      const float2 z = __fmul2_rn(make_float2(__uint_as_float(sr[2 * cp]), __uint_as_float(sr[2 * cp + 1])), sc2);
+      float2 z = __fmul2_rn(make_float2(__uint_as_float(sr[2 * cp]), __uint_as_float(sr[2 * cp + 1])), sc2);
+      if (op >= 3) {
+        z.x = ptx::act(op, z.x);
+        z.y = ptx::act(op, z.y);
+      }
       pk[c] = ptx::pack2<BF16>(z.x, z.y);
     }
     ptx::tmem_st16(tS + ch * 16, pk);
@@ -719,7 +724,7 @@ __global__ void __launch_bounds__(kT4Threads, 1)
         ptx::tmem_wait_ld();
         if (p.op != 2) {
           // NONE / SCALE: padded keys have S = 0 and zero V rows (TMA fill), no masking needed
-          t4_cvt_row<BF16>(tS, sr, sc);
+          t4_cvt_row<BF16>(tS, sr, sc, p.op);
           ptx::tmem_wait_st();
           ptx::tc_fence_before();
           ptx::mbar_arrive(&p_full[b]);

@@ -556,7 +556,7 @@ __global__ void __launch_bounds__(kT5Threads, 1)
           // NONE / SCALE: padded keys have S = 0 and zero V rows (TMA fill), no masking needed
           if (g > 0) ptx::mbar_wait(&p_free[x], ph ^ 1u);   // G2_x(g - 1) has read P_x
           ptx::tc_fence_after();
-          t4_cvt_row<BF16>(tP, sr, sc);
+          t4_cvt_row<BF16>(tP, sr, sc, p.op);
         } else {
           float mx;
           if (full)

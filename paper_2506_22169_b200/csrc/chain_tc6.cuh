@@ -67,7 +67,7 @@ __device__ __forceinline__ void t6_exp_half(uint32_t (&pk)[32], const uint32_t (
 
 // NONE / SCALE: P = cvt(scale · S) for a 64-column half row
 template <bool BF16>
-__device__ __forceinline__ void t6_cvt_half(uint32_t tP, const uint32_t (&sr)[64], float sc) {
+__device__ __forceinline__ void t6_cvt_half(uint32_t tP, const uint32_t (&sr)[64], float sc, int op) {
   const float2 sc2 = make_float2(sc, sc);
 #pragma unroll
   for (int ch = 0; ch < 2; ++ch) {
@@ -75,7 +75,11 @@ __device__ __forceinline__ void t6_cvt_half(uint32_t tP, const uint32_t (&sr)[64
 #pragma unroll
     for (int c = 0; c < 16; ++c) {
       const int cp = ch * 16 + c;
-      const float2 z = __fmul2_rn(make_float2(__uint_as_float(sr[2 * cp]), __uint_as_float(sr[2 * cp + 1])), sc2);
+      float2 z = __fmul2_rn(make_float2(__uint_as_float(sr[2 * cp]), __uint_as_float(sr[2 * cp + 1])), sc2);
+      if (op >= 3) {
+        z.x = ptx::act(op, z.x);
+        z.y = ptx::act(op, z.y);
+      }
       pk[c] = ptx::pack2<BF16>(z.x, z.y);
     }
     ptx::tmem_st16(tP + ch * 16, pk);
@@ -526,7 +530,7 @@ __global__ void __launch_bounds__(kT6Threads, 1)
           // NONE / SCALE: padded keys have S = 0 and zero V rows (TMA fill), no masking needed
           if (g > 0) ptx::mbar_wait(&p_free[x], ph ^ 1u);   // G2_x(g - 1) has read P_x
           ptx::tc_fence_after();
-          t6_cvt_half<BF16>(tP, sr, sc);
+          t6_cvt_half<BF16>(tP, sr, sc, p.op);
         } else {
           float mx;
           if (full)

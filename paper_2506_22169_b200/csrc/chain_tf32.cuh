@@ -32,7 +32,7 @@ struct Tf32Params {
   int32_t M, N, K, L;
   int32_t KP;    // K padded to a multiple of 8 (the TF32 MMA K step), <= 64
   int32_t TLP;   // L padded to a multiple of 16 (the MMA N granularity), <= 64
-  int32_t op;    // 0 none, 1 scale, 2 softmax
+  int32_t op;    // 0 none, 1 scale, 2 softmax, 3 relu, 4 gelu
   int32_t causal; // softmax: key n visible to row m only if n <= m (R18)
   float scale;   // softmax: scale * log2(e); SCALE: the multiplier
   int32_t b_layout;
@@ -234,7 +234,8 @@ __global__ void __launch_bounds__(kTf32Threads, 1)
       l_run += sum;
     } else {
 #pragma unroll
-      for (int c = 0; c < kTf32BN; ++c) pv[c] = p.op == 1 ? p.scale * __uint_as_float(s[c]) : __uint_as_float(s[c]);
+      for (int c = 0; c < kTf32BN; ++c)
+        pv[c] = p.op == 0 ? __uint_as_float(s[c]) : ptx::act(p.op, p.scale * __uint_as_float(s[c]));
     }
 #pragma unroll
     for (int c0 = 0; c0 < kTf32BN; c0 += 16) {

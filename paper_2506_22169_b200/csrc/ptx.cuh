@@ -364,6 +364,14 @@ __device__ __forceinline__ float min3(float a, float b, float c) {
   return d;
 }
 
+// Elementwise inter-ops on x = scale·S (mbci.h: 3 RELU, 4 GELU with the exact erf form; other op
+// codes pass x through).  DESIGN.md R19.
+__device__ __forceinline__ float act(int op, float x) {
+  if (op == 3) return fmaxf(x, 0.0f);
+  if (op == 4) return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f));
+  return x;
+}
+
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));

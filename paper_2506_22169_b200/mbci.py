@@ -26,7 +26,9 @@ MBCI_MASK_NONE, MBCI_MASK_KEY_PADDING, MBCI_MASK_CAUSAL, MBCI_MASK_CAUSAL_KEY_PA
 MBCI_OK, MBCI_ERR_INVALID, MBCI_ERR_UNSUPPORTED, MBCI_ERR_CUDA, MBCI_ERR_NOMEM = 0, 1, 2, 3, 4
 
 DTYPES = {"f32": MBCI_F32, "f16": MBCI_F16, "bf16": MBCI_BF16}
-OPS = {"none": MBCI_OP_NONE, "scale": MBCI_OP_SCALE, "softmax": MBCI_OP_SOFTMAX}
+MBCI_OP_RELU, MBCI_OP_GELU = 3, 4
+OPS = {"none": MBCI_OP_NONE, "scale": MBCI_OP_SCALE, "softmax": MBCI_OP_SOFTMAX, "relu": MBCI_OP_RELU,
+       "gelu": MBCI_OP_GELU}
 
 
 class mbci_chain_desc_t(ctypes.Structure):
