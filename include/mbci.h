@@ -87,7 +87,8 @@ typedef struct {
   int32_t b_layout;     /* 0 or 1, see above */
   int64_t ld_a, ld_b, ld_d, ld_e;
   int64_t bs_a, bs_b, bs_d, bs_e;
-  int32_t tune;         /* 0: analytical model picks the plan; 1: also time the top-8 at create */
+  int32_t tune;         /* 0: analytical model picks the plan; 1: also time the top-8 at create;
+                           2: PAPER.md Algorithm 1 (mbci_plan_search with GPU timing) at create */
 } mbci_chain_desc_t;
 
 /* Hardware description used by the tile selector (Eqs. 2-5). */
@@ -176,6 +177,34 @@ const char* mbci_last_error(void);   /* thread-local; valid until the next call 
 int32_t mbci_abi_version(void);
 
 /* ---- tile selector (host only; never touches a GPU) ------------------------------------- */
+
+/* PAPER.md Algorithm 1 (§IV-B) over the legal plans of desc on hw: a population of N
+ * random candidates, each round ranked by the analytical model (model 0: the paper's t_estm,
+ * Eqs. 2-5; 1: the B200 score t_b200), the n best-estimated measured by `measure` (seconds; a
+ * plan is measured once), stop when |top1 - best| / best < eps (returning top1, as the paper's
+ * pseudocode), else mutate: N draws weighted by 1 / estimate, each moving one tile parameter
+ * (BN, TL or the pipeline depth) to an adjacent legal value; the kernel family (the tiling
+ * expression) never mutates.  Host only: `measure` decides what a measurement is (GPU timing in
+ * mbci_chain_create with tune = 2).  Defaults (params NULL): N 512, n 8, eps 0.01, seed 1,
+ * max_rounds 64, model 0.  round_log (optional) receives 3 doubles per round: best estimate,
+ * measured top 1, best measured so far.  Errors: INVALID, UNSUPPORTED (no legal plan). */
+typedef struct {
+  int32_t N, n;
+  double eps;
+  uint64_t seed;
+  int32_t max_rounds, model;
+} mbci_search_params_t;
+typedef double (*mbci_measure_fn)(const mbci_plan_t* plan, void* user);
+typedef struct {
+  int32_t rounds, measurements, space_size;
+  double best_measured, history_min;
+} mbci_search_result_t;
+mbci_status_t mbci_plan_search(const mbci_chain_desc_t* desc, const mbci_hw_t* hw,
+                               const mbci_search_params_t* params, mbci_measure_fn measure, void* user,
+                               mbci_plan_t* best, mbci_search_result_t* result, double* round_log);
+
+/* Rounds and measurements of the Algorithm-1 search a tune = 2 handle ran at create (0, 0 otherwise). */
+mbci_status_t mbci_chain_search_stats(mbci_chain_t h, int32_t* rounds, int32_t* measurements);
 
 /* Default B200 hardware description: W and P from MEASURED_PEAKS-style figures, 148 SMs,
  * 232448 B shared memory, 512 TMEM columns, 16 ex2/clk/SM at 1.965 GHz. */

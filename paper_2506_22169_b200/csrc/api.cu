@@ -17,6 +17,7 @@
 #include "../../include/mbci.h"
 #include "chain_tc6.cuh"   // kT5Threads, kT6Threads (the kernels are instantiated in k_*.cu)
 #include "kernels.h"
+#include "search.h"
 #include "selector.h"
 
 using namespace mbci;
@@ -52,7 +53,7 @@ mbci_status_t normalize(const mbci_chain_desc_t* in, mbci_chain_desc_t* d) {
   if (d->mask != MBCI_MASK_NONE && d->op != MBCI_OP_SOFTMAX)
     return fail(MBCI_ERR_INVALID, "masks require op SOFTMAX");
   if (d->b_layout != 0 && d->b_layout != 1) return fail(MBCI_ERR_INVALID, "bad b_layout %d", d->b_layout);
-  if (d->tune != 0 && d->tune != 1) return fail(MBCI_ERR_INVALID, "bad tune %d", d->tune);
+  if (d->tune < 0 || d->tune > 2) return fail(MBCI_ERR_INVALID, "bad tune %d", d->tune);
   if (d->K > kMaxK || d->L > kMaxL)
     return fail(MBCI_ERR_UNSUPPORTED, "K=%lld L=%lld: this build takes K, L <= %lld",
                 (long long)d->K, (long long)d->L, (long long)kMaxK);
@@ -180,6 +181,7 @@ struct mbci_chain {
   Tc4Kernel tc4 = nullptr;   // kernel 4
   Tc5Kernel tc5 = nullptr;   // kernels 5 / 6 (same parameter block, plus E's tensor map)
   int32_t threads = 0;       // block size of the persistent kernels
+  int32_t search_rounds = 0, search_measurements = 0;   // tune = 2 (Algorithm 1) statistics
   Tc4Params tp4{};
   Tf32Params tp7{};          // kernel 7 (fp32, 3xTF32)
   int32_t grid2 = 0;
@@ -485,86 +487,118 @@ __global__ void k_tune_fill(uint16_t* x, int64_t n, uint32_t seed, int bf16) {
   }
 }
 
-mbci_status_t tune_plan(mbci_chain* h, const std::vector<mbci_plan_t>& plans) {
-  // PAPER.md Alg. 1 lines 5-9: estimate all, measure the top n = 8.  A candidate
-  // whose set-up or launch fails is skipped, never timed.
-  const mbci_chain_desc_t& d = h->d;
-  const int64_t s = elem_size(d);
-  const int64_t b_rows = d.b_layout == 0 ? d.K : d.N, b_cols = d.b_layout == 0 ? d.N : d.K;
-  const size_t nA = span_elems(d.batch, d.M, d.K, d.ld_a, d.bs_a) * s;
-  const size_t nB = span_elems(d.batch, b_rows, b_cols, d.ld_b, d.bs_b) * s;
-  const size_t nD = span_elems(d.batch, d.N, d.L, d.ld_d, d.bs_d) * s;
-  const size_t nE = span_elems(d.batch, d.M, d.L, d.ld_e, d.bs_e) * s;
+// Timing bench for plan selection (desc.tune = 1: measure a shortlist; 2: PAPER.md Alg. 1).
+// Scratch inputs are seeded non-zero values; a candidate whose set-up or launch fails is never
+// timed (+inf); a device fault poisons the context and is reported.
+struct TuneBench {
+  mbci_chain* h;
   void *A = nullptr, *B = nullptr, *D = nullptr, *E = nullptr;
   int32_t* V = nullptr;
   cudaStream_t st = nullptr;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
-  mbci_status_t rc = MBCI_OK;
-  float best = 1e30f;
-  int best_i = -1;
-  const int n_try = std::min<int>(8, (int)plans.size());
-  if (cudaMalloc(&A, std::max<size_t>(nA, 16)) != cudaSuccess || cudaMalloc(&B, std::max<size_t>(nB, 16)) != cudaSuccess ||
-      cudaMalloc(&D, std::max<size_t>(nD, 16)) != cudaSuccess || cudaMalloc(&E, std::max<size_t>(nE, 16)) != cudaSuccess ||
-      cudaMalloc(&V, std::max<int64_t>(d.batch, 1) * 4) != cudaSuccess) {
-    rc = fail(MBCI_ERR_NOMEM, "tune scratch allocation failed");
-    goto done;
-  }
-  cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
-  if (s == 2) {
-    k_tune_fill<<<256, 256, 0, st>>>((uint16_t*)A, (int64_t)(nA / 2), 1u, d.dtype == MBCI_BF16);
-    k_tune_fill<<<256, 256, 0, st>>>((uint16_t*)B, (int64_t)(nB / 2), 2u, d.dtype == MBCI_BF16);
-    k_tune_fill<<<256, 256, 0, st>>>((uint16_t*)D, (int64_t)(nD / 2), 3u, d.dtype == MBCI_BF16);
-  } else {
-    cudaMemsetAsync(A, 0, nA, st);
-    cudaMemsetAsync(B, 0, nB, st);
-    cudaMemsetAsync(D, 0, nD, st);
-  }
-  {
+  mbci_status_t fault = MBCI_OK;
+
+  explicit TuneBench(mbci_chain* hh) : h(hh) {}
+  mbci_status_t init() {
+    const mbci_chain_desc_t& d = h->d;
+    const int64_t s = elem_size(d);
+    const int64_t b_rows = d.b_layout == 0 ? d.K : d.N, b_cols = d.b_layout == 0 ? d.N : d.K;
+    const size_t nA = span_elems(d.batch, d.M, d.K, d.ld_a, d.bs_a) * s;
+    const size_t nB = span_elems(d.batch, b_rows, b_cols, d.ld_b, d.bs_b) * s;
+    const size_t nD = span_elems(d.batch, d.N, d.L, d.ld_d, d.bs_d) * s;
+    const size_t nE = span_elems(d.batch, d.M, d.L, d.ld_e, d.bs_e) * s;
+    if (cudaMalloc(&A, std::max<size_t>(nA, 16)) != cudaSuccess || cudaMalloc(&B, std::max<size_t>(nB, 16)) != cudaSuccess ||
+        cudaMalloc(&D, std::max<size_t>(nD, 16)) != cudaSuccess || cudaMalloc(&E, std::max<size_t>(nE, 16)) != cudaSuccess ||
+        cudaMalloc(&V, std::max<int64_t>(d.batch, 1) * 4) != cudaSuccess)
+      return fail(MBCI_ERR_NOMEM, "tune scratch allocation failed");
+    cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    if (s == 2) {
+      k_tune_fill<<<256, 256, 0, st>>>((uint16_t*)A, (int64_t)(nA / 2), 1u, d.dtype == MBCI_BF16);
+      k_tune_fill<<<256, 256, 0, st>>>((uint16_t*)B, (int64_t)(nB / 2), 2u, d.dtype == MBCI_BF16);
+      k_tune_fill<<<256, 256, 0, st>>>((uint16_t*)D, (int64_t)(nD / 2), 3u, d.dtype == MBCI_BF16);
+    } else {
+      cudaMemsetAsync(A, 0, nA, st);
+      cudaMemsetAsync(B, 0, nB, st);
+      cudaMemsetAsync(D, 0, nD, st);
+    }
     std::vector<int32_t> hv(std::max<int64_t>(d.batch, 1), (int32_t)d.N);
     cudaMemcpyAsync(V, hv.data(), hv.size() * 4, cudaMemcpyHostToDevice, st);
     cudaStreamSynchronize(st);
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    return MBCI_OK;
   }
-  cudaEventCreate(&e0);
-  cudaEventCreate(&e1);
-  for (int i = 0; i < n_try; ++i) {
-    h->plan = plans[i];
+  // seconds per launch of `plan` (2 warm-up + 5 timed launches), +inf if it cannot run
+  double time_plan(const mbci_plan_t& plan) {
+    if (fault != MBCI_OK) return 1e30;
+    h->plan = plan;
     for (auto& c : h->cache) c = MapCacheEntry{};
-    if (setup_plan(h) != MBCI_OK) continue;
+    if (setup_plan(h) != MBCI_OK) return 1e30;
     bool ok = true;
     for (int w = 0; w < 2 && ok; ++w) ok = launch(h, A, B, D, E, V, st) == MBCI_OK;
     cudaEventRecord(e0, st);
     for (int r = 0; r < 5 && ok; ++r) ok = launch(h, A, B, D, E, V, st) == MBCI_OK;
     cudaEventRecord(e1, st);
     cudaError_t ce = cudaEventSynchronize(e1);
-    if (ce != cudaSuccess) {   // a device fault poisons the context: report it
-      rc = cuda_fail(ce, "tuning run");
-      goto done;
+    if (ce != cudaSuccess) {
+      fault = cuda_fail(ce, "tuning run");
+      return 1e30;
     }
-    if (!ok || cudaGetLastError() != cudaSuccess) continue;
+    if (!ok || cudaGetLastError() != cudaSuccess) return 1e30;
     float ms = 0.f;
     cudaEventElapsedTime(&ms, e0, e1);
-    if (ms < best) {
-      best = ms;
+    return ms * 1e-3 / 5.0;
+  }
+  ~TuneBench() {
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    if (st) cudaStreamDestroy(st);
+    cudaFree(A);
+    cudaFree(B);
+    cudaFree(D);
+    cudaFree(E);
+    cudaFree(V);
+  }
+};
+
+mbci_status_t tune_plan(mbci_chain* h, const std::vector<mbci_plan_t>& plans) {
+  // PAPER.md Alg. 1 lines 5-9 in one round: estimate all, measure the top n = 8.
+  TuneBench tb(h);
+  mbci_status_t rc = tb.init();
+  if (rc != MBCI_OK) return rc;
+  double best = 1e30;
+  int best_i = -1;
+  const int n_try = std::min<int>(8, (int)plans.size());
+  for (int i = 0; i < n_try; ++i) {
+    const double t = tb.time_plan(plans[i]);
+    if (tb.fault != MBCI_OK) return tb.fault;
+    if (t < best) {
+      best = t;
       best_i = i;
     }
   }
-  if (best_i < 0) {
-    rc = fail(MBCI_ERR_UNSUPPORTED, "tuning: no candidate plan launched successfully");
-    goto done;
-  }
+  if (best_i < 0) return fail(MBCI_ERR_UNSUPPORTED, "tuning: no candidate plan launched successfully");
   h->plan = plans[best_i];
   for (auto& c : h->cache) c = MapCacheEntry{};
-  rc = setup_plan(h);
-done:
-  if (e0) cudaEventDestroy(e0);
-  if (e1) cudaEventDestroy(e1);
-  if (st) cudaStreamDestroy(st);
-  cudaFree(A);
-  cudaFree(B);
-  cudaFree(D);
-  cudaFree(E);
-  cudaFree(V);
-  return rc;
+  return setup_plan(h);
+}
+
+// desc.tune = 2: PAPER.md Algorithm 1 over every legal plan, measured on the handle's device.
+mbci_status_t search_plan(mbci_chain* h, const std::vector<mbci_plan_t>& plans) {
+  TuneBench tb(h);
+  mbci_status_t rc = tb.init();
+  if (rc != MBCI_OK) return rc;
+  SearchParams sp;   // N = 512, n = 8, eps = 1 %, seed 1, 64 rounds, the paper's t_estm
+  mbci_plan_t best{};
+  SearchLog log;
+  const int r = alg1_search(plans, sp, [&](const mbci_plan_t& p) { return tb.time_plan(p); }, &best, &log);
+  if (tb.fault != MBCI_OK) return tb.fault;
+  if (r != 0 || log.best_measured >= 1e29) return fail(MBCI_ERR_UNSUPPORTED, "search: no candidate ran");
+  h->plan = best;
+  h->search_rounds = (int32_t)log.rounds.size();
+  h->search_measurements = log.measurements;
+  for (auto& c : h->cache) c = MapCacheEntry{};
+  return setup_plan(h);
 }
 
 // Restores the caller's current device on scope exit (the ABI never leaves it changed).
@@ -643,6 +677,8 @@ mbci_status_t create_impl(const mbci_chain_desc_t* desc, int device, const mbci_
     }
     if (shortlist.size() > 8) shortlist.resize(8);
     s = tune_plan(h, shortlist);
+  } else if (s == MBCI_OK && !forced && d.tune == 2 && plans.size() > 1) {
+    s = search_plan(h, plans);   // PAPER.md Algorithm 1
   }
   if (s != MBCI_OK) {
     delete h;
@@ -807,6 +843,53 @@ mbci_status_t mbci_plan_select(const mbci_chain_desc_t* desc, const mbci_hw_t* h
   if (!out) return fail(MBCI_ERR_INVALID, "out is NULL");
   int32_t n = 0;
   return mbci_plan_enumerate(desc, hw, out, 1, &n);
+}
+
+mbci_status_t mbci_plan_search(const mbci_chain_desc_t* desc, const mbci_hw_t* hw,
+                               const mbci_search_params_t* params, mbci_measure_fn measure, void* user,
+                               mbci_plan_t* best, mbci_search_result_t* result, double* round_log) {
+  if (!measure || !best) return fail(MBCI_ERR_INVALID, "measure and best must be non-NULL");
+  mbci_chain_desc_t d;
+  mbci_status_t s = normalize(desc, &d);
+  if (s != MBCI_OK) return s;
+  mbci_hw_t hh;
+  if (hw) hh = *hw; else hw_default(&hh);
+  std::vector<mbci_plan_t> space;
+  enumerate_plans(d, hh, space);
+  if (space.empty()) return fail(MBCI_ERR_UNSUPPORTED, "no legal plan");
+  SearchParams sp;
+  if (params) {
+    sp.N = params->N;
+    sp.n = params->n;
+    sp.eps = params->eps;
+    sp.seed = params->seed;
+    sp.max_rounds = params->max_rounds;
+    sp.model = params->model;
+  }
+  SearchLog log;
+  const int r = alg1_search(space, sp, [&](const mbci_plan_t& p) { return measure(&p, user); }, best, &log);
+  if (r != 0) return fail(MBCI_ERR_INVALID, "bad search parameters");
+  if (result) {
+    result->rounds = (int32_t)log.rounds.size();
+    result->measurements = log.measurements;
+    result->space_size = (int32_t)space.size();
+    result->best_measured = log.best_measured;
+    result->history_min = log.history_min;
+  }
+  if (round_log)
+    for (size_t i = 0; i < log.rounds.size(); ++i) {
+      round_log[3 * i] = log.rounds[i].best_estimated;
+      round_log[3 * i + 1] = log.rounds[i].top1_measured;
+      round_log[3 * i + 2] = log.rounds[i].best_measured;
+    }
+  return MBCI_OK;
+}
+
+mbci_status_t mbci_chain_search_stats(mbci_chain_t h, int32_t* rounds, int32_t* measurements) {
+  if (!h) return fail(MBCI_ERR_INVALID, "handle is NULL");
+  if (rounds) *rounds = h->search_rounds;
+  if (measurements) *measurements = h->search_measurements;
+  return MBCI_OK;
 }
 
 mbci_status_t mbci_model_terms(int64_t batch, int64_t M, int64_t N, int64_t K, int64_t L, int64_t TM,

@@ -82,17 +82,34 @@ _lib.mbci_plan_enumerate.argtypes = [_P(mbci_chain_desc_t), _P(mbci_hw_t), _P(mb
                                      _P(ctypes.c_int32)]
 _lib.mbci_plan_select.argtypes = [_P(mbci_chain_desc_t), _P(mbci_hw_t), _P(mbci_plan_t)]
 _lib.mbci_model_terms.argtypes = [ctypes.c_int64] * 9 + [ctypes.c_int32, _P(mbci_hw_t), _P(ctypes.c_double)]
+
+
+class mbci_search_params_t(ctypes.Structure):
+    _fields_ = [("N", ctypes.c_int32), ("n", ctypes.c_int32), ("eps", ctypes.c_double), ("seed", ctypes.c_uint64),
+                ("max_rounds", ctypes.c_int32), ("model", ctypes.c_int32)]
+
+
+class mbci_search_result_t(ctypes.Structure):
+    _fields_ = [("rounds", ctypes.c_int32), ("measurements", ctypes.c_int32), ("space_size", ctypes.c_int32),
+                ("best_measured", ctypes.c_double), ("history_min", ctypes.c_double)]
+
+
+mbci_measure_fn = ctypes.CFUNCTYPE(ctypes.c_double, _P(mbci_plan_t), _vp)
+_lib.mbci_plan_search.argtypes = [_P(mbci_chain_desc_t), _P(mbci_hw_t), _P(mbci_search_params_t), mbci_measure_fn,
+                                  _vp, _P(mbci_plan_t), _P(mbci_search_result_t), _P(ctypes.c_double)]
+_lib.mbci_chain_search_stats.argtypes = [_vp, _P(ctypes.c_int32), _P(ctypes.c_int32)]
 for _f in ("mbci_chain_create", "mbci_chain_create_with_plan", "mbci_chain_run", "mbci_chain_run_host",
            "mbci_chain_set_trace",
            "mbci_chain_destroy", "mbci_chain_plan", "mbci_chain_describe", "mbci_plan_enumerate",
-           "mbci_plan_select", "mbci_model_terms"):
+           "mbci_plan_select", "mbci_model_terms", "mbci_plan_search", "mbci_chain_search_stats"):
     getattr(_lib, _f).restype = _st
 
 EXPORTED = ["mbci_chain_create", "mbci_chain_create_with_plan", "mbci_chain_run", "mbci_chain_run_host",
             "mbci_chain_destroy", "mbci_chain_plan", "mbci_chain_describe", "mbci_chain_launches_per_run",
             "mbci_chain_set_trace",
             "mbci_status_string", "mbci_last_error", "mbci_abi_version", "mbci_hw_default",
-            "mbci_plan_enumerate", "mbci_plan_select", "mbci_model_terms"]
+            "mbci_plan_enumerate", "mbci_plan_select", "mbci_model_terms", "mbci_plan_search",
+            "mbci_chain_search_stats"]
 
 # ---- same names as the C ABI ---------------------------------------------------------------
 mbci_chain_create = _lib.mbci_chain_create
@@ -111,6 +128,22 @@ mbci_hw_default = _lib.mbci_hw_default
 mbci_plan_enumerate = _lib.mbci_plan_enumerate
 mbci_plan_select = _lib.mbci_plan_select
 mbci_model_terms = _lib.mbci_model_terms
+mbci_plan_search = _lib.mbci_plan_search
+mbci_chain_search_stats = _lib.mbci_chain_search_stats
+
+
+def plan_search(desc, measure, hw=None, N=512, n=8, eps=0.01, seed=1, max_rounds=64, model=0):
+    """PAPER.md Algorithm 1 through the C ABI; `measure(plan) -> seconds` is a Python callable.
+    Returns (status, best plan, result struct, per-round log [(best_est, top1_meas, best_meas)])."""
+    params = mbci_search_params_t(N, n, eps, seed, max_rounds, model)
+    cb = mbci_measure_fn(lambda pp, _u: float(measure(pp.contents)))
+    best = mbci_plan_t()
+    res = mbci_search_result_t()
+    log = (ctypes.c_double * (3 * max(1, max_rounds)))()
+    st = mbci_plan_search(ctypes.byref(desc), None if hw is None else ctypes.byref(hw), ctypes.byref(params), cb,
+                          None, ctypes.byref(best), ctypes.byref(res), log)
+    rounds = [(log[3 * i], log[3 * i + 1], log[3 * i + 2]) for i in range(res.rounds)] if st == MBCI_OK else []
+    return st, best, res, rounds
 
 
 class MbciError(RuntimeError):
