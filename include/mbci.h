@@ -146,8 +146,10 @@ mbci_status_t mbci_chain_run(mbci_chain_t h, const void* A, const void* B, const
 
 /* End-to-end convenience: A, B, D, E and valid_len are HOST pointers (pinned memory gives
  * asynchronous copies).  Copies the inputs to handle-owned device buffers (allocated on
- * first use and kept), runs the chain, copies E back, and synchronises `stream` before
- * returning.  Same layouts, strides and errors as mbci_chain_run, plus NOMEM. */
+ * first use and kept), runs the chain, copies E back, and returns when E is on the host.
+ * The batch is cut into up to 4 chunks pipelined over two handle-owned streams (after the work
+ * already queued on `stream`): the H2D copy of one chunk, the kernel of another and the D2H copy
+ * of a third overlap.  Same layouts, strides and errors as mbci_chain_run, plus NOMEM. */
 mbci_status_t mbci_chain_run_host(mbci_chain_t h, const void* A, const void* B, const void* D,
                                   void* E, const int32_t* valid_len, void* stream);
 

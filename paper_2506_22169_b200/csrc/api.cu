@@ -171,6 +171,15 @@ struct MapCacheEntry {
 
 }  // namespace
 
+constexpr int kHostChunks = 8;   // run_host pipeline depth (batch chunks), at most
+
+// run_host chunk count (MBCI_HOST_CHUNKS overrides, 1 = the serial single-stream pipeline)
+int host_chunks() {
+  const char* e = getenv("MBCI_HOST_CHUNKS");
+  if (e) return std::max(1, std::min(kHostChunks, atoi(e)));
+  return 4;
+}
+
 struct mbci_chain {
   mbci_chain_desc_t d{};
   mbci_plan_t plan{};
@@ -193,6 +202,11 @@ struct mbci_chain {
   void *dA = nullptr, *dB = nullptr, *dD = nullptr, *dE = nullptr;
   int32_t* dV = nullptr;
   size_t nA = 0, nB = 0, nD = 0, nE = 0;
+  cudaStream_t cst[3] = {nullptr, nullptr, nullptr};   // run_host: H2D, kernels, D2H
+  cudaEvent_t cev[3 + 2 * kHostChunks] = {};           // run_host: fork, per chunk (inputs in, kernel done), joins
+  cudaGraphExec_t hg_exec = nullptr;                   // run_host: the captured chunk pipeline
+  const void* hg_key[5] = {};                          // ... for these host pointers (A, B, D, E, valid_len)
+  mbci_chain* sub[2] = {nullptr, nullptr};    // run_host: same plan on the chunk batch sizes
 };
 
 namespace {
@@ -714,15 +728,17 @@ mbci_status_t mbci_chain_run_host(mbci_chain_t h, const void* A, const void* B, 
   if (!h) return fail(MBCI_ERR_INVALID, "handle is NULL");
   const mbci_chain_desc_t& d = h->d;
   if (d.batch == 0 || d.M == 0 || d.L == 0) return MBCI_OK;
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (!E) return fail(MBCI_ERR_INVALID, "E is NULL");
+  if ((d.mask & MBCI_MASK_KEY_PADDING) && !valid_len) return fail(MBCI_ERR_INVALID, "mask KEY_PADDING needs valid_len");
+  cudaStream_t ust = reinterpret_cast<cudaStream_t>(stream);
   const int64_t s = elem_size(d);
   const int64_t b_rows = d.b_layout == 0 ? d.K : d.N, b_cols = d.b_layout == 0 ? d.N : d.K;
-  const size_t nA = span_elems(d.batch, d.M, d.K, d.ld_a, d.bs_a) * s;
-  const size_t nB = span_elems(d.batch, b_rows, b_cols, d.ld_b, d.bs_b) * s;
-  const size_t nD = span_elems(d.batch, d.N, d.L, d.ld_d, d.bs_d) * s;
-  const size_t nE = span_elems(d.batch, d.M, d.L, d.ld_e, d.bs_e) * s;
   DeviceGuard guard(h->device);
-  cudaError_t e = cudaSuccess;
+  auto span_bytes = [&](int64_t nb, int64_t rows, int64_t cols, int64_t ld, int64_t bs) {
+    return (size_t)(span_elems(nb, rows, cols, ld, bs) * s);
+  };
+  const size_t nA = span_bytes(d.batch, d.M, d.K, d.ld_a, d.bs_a), nB = span_bytes(d.batch, b_rows, b_cols, d.ld_b, d.bs_b);
+  const size_t nD = span_bytes(d.batch, d.N, d.L, d.ld_d, d.bs_d), nE = span_bytes(d.batch, d.M, d.L, d.ld_e, d.bs_e);
   auto ensure = [&](void** p, size_t* have, size_t need) -> bool {
     if (*have >= need && *p) return true;
     if (*p) cudaFree(*p);
@@ -736,34 +752,163 @@ mbci_status_t mbci_chain_run_host(mbci_chain_t h, const void* A, const void* B, 
   if (!ensure(&h->dA, &h->nA, nA) || !ensure(&h->dB, &h->nB, nB) || !ensure(&h->dD, &h->nD, nD) ||
       !ensure(&h->dE, &h->nE, nE) || !ensure((void**)&h->dV, &nV_have, (size_t)d.batch * 4))
     return fail(MBCI_ERR_NOMEM, "device scratch allocation failed");
-  if (nA && (e = cudaMemcpyAsync(h->dA, A, nA, cudaMemcpyHostToDevice, st)) != cudaSuccess) return cuda_fail(e, "H2D A");
-  if (nB && (e = cudaMemcpyAsync(h->dB, B, nB, cudaMemcpyHostToDevice, st)) != cudaSuccess) return cuda_fail(e, "H2D B");
-  if (nD && (e = cudaMemcpyAsync(h->dD, D, nD, cudaMemcpyHostToDevice, st)) != cudaSuccess) return cuda_fail(e, "H2D D");
-  const int32_t* dv = nullptr;
-  if (d.mask & MBCI_MASK_KEY_PADDING) {
-    if (!valid_len) return fail(MBCI_ERR_INVALID, "mask KEY_PADDING needs valid_len");
-    if ((e = cudaMemcpyAsync(h->dV, valid_len, d.batch * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess)
-      return cuda_fail(e, "H2D valid_len");
-    dv = h->dV;
+
+  // Enqueue the copies and kernels of batch rows [b0, b0 + nb): H2D on s_in, the kernel on s_k
+  // (after the inputs landed), D2H on s_out (after the kernel).  One stream for all three gives the
+  // plain serial pipeline.
+  auto enqueue = [&](mbci_chain* run, int64_t b0, int64_t nb, cudaStream_t s_in, cudaStream_t s_k,
+                     cudaStream_t s_out, cudaEvent_t in_ev, cudaEvent_t k_ev) -> mbci_status_t {
+    cudaError_t e = cudaSuccess;
+    auto h2d = [&](void* dst, const void* src, int64_t rows, int64_t cols, int64_t ld, int64_t bs) {
+      const size_t off = (size_t)(b0 * bs * s), len = span_bytes(nb, rows, cols, ld, bs);
+      if (len && e == cudaSuccess)
+        e = cudaMemcpyAsync((char*)dst + off, (const char*)src + off, len, cudaMemcpyHostToDevice, s_in);
+    };
+    if (d.K > 0 && d.N > 0) {
+      h2d(h->dA, A, d.M, d.K, d.ld_a, d.bs_a);
+      h2d(h->dB, B, b_rows, b_cols, d.ld_b, d.bs_b);
+    }
+    if (d.N > 0) h2d(h->dD, D, d.N, d.L, d.ld_d, d.bs_d);
+    const int32_t* dv = nullptr;
+    if (d.mask & MBCI_MASK_KEY_PADDING) {
+      if (e == cudaSuccess) e = cudaMemcpyAsync(h->dV + b0, valid_len + b0, nb * 4, cudaMemcpyHostToDevice, s_in);
+      dv = h->dV + b0;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "run_host H2D");
+    if (s_k != s_in) {
+      cudaEventRecord(in_ev, s_in);
+      cudaStreamWaitEvent(s_k, in_ev, 0);
+    }
+    mbci_status_t rs = launch(run, (const char*)h->dA + b0 * d.bs_a * s, (const char*)h->dB + b0 * d.bs_b * s,
+                              (const char*)h->dD + b0 * d.bs_d * s, (char*)h->dE + b0 * d.bs_e * s, dv, s_k);
+    if (rs != MBCI_OK) return rs;
+    if (s_out != s_k) {
+      cudaEventRecord(k_ev, s_k);
+      cudaStreamWaitEvent(s_out, k_ev, 0);
+    }
+    // E back row by row (2-D copies) so host bytes between rows are never written
+    char* he = (char*)E + b0 * d.bs_e * s;
+    const char* de = (const char*)h->dE + b0 * d.bs_e * s;
+    if (d.bs_e == d.M * d.ld_e) {
+      e = cudaMemcpy2DAsync(he, d.ld_e * s, de, d.ld_e * s, d.L * s, nb * d.M, cudaMemcpyDeviceToHost, s_out);
+    } else {
+      for (int64_t b = 0; b < nb && e == cudaSuccess; ++b)
+        e = cudaMemcpy2DAsync(he + b * d.bs_e * s, d.ld_e * s, de + b * d.bs_e * s, d.ld_e * s, d.L * s, d.M,
+                              cudaMemcpyDeviceToHost, s_out);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "run_host D2H E");
+    return MBCI_OK;
+  };
+
+  // Pinned host buffers: the batch is cut into up to kHostChunks chunks pipelined over three
+  // handle-owned streams (all H2D copies back to back — PCIe-bound —, each chunk's kernel once its
+  // inputs landed, each chunk's D2H once its kernel ran), captured ONCE into a CUDA graph per set of
+  // host pointers and replayed on `stream`: one graph launch per call instead of ~8 API calls per
+  // chunk.  A chunk runs the handle's plan on its batch rows through a sub-handle (created once).
+  auto pinned = [](const void* p) {
+    if (!p) return true;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+  };
+  const bool graph_ok = pinned(A) && pinned(B) && pinned(D) && pinned(E) &&
+                        (!(d.mask & MBCI_MASK_KEY_PADDING) || pinned(valid_len)) && host_chunks() > 1;
+  if (graph_ok) {
+    const void* key[5] = {A, B, D, E, valid_len};
+    bool hit = h->hg_exec != nullptr;
+    for (int i = 0; i < 5 && hit; ++i) hit = h->hg_key[i] == key[i];
+    if (!hit) {
+      if (h->hg_exec) {
+        cudaGraphExecDestroy(h->hg_exec);
+        h->hg_exec = nullptr;
+      }
+      const int64_t n_chunks = std::min<int64_t>(d.batch, host_chunks());
+      const int64_t cb = (d.batch + n_chunks - 1) / n_chunks;
+      for (int i = 0; i < 3; ++i)
+        if (!h->cst[i] && cudaStreamCreateWithFlags(&h->cst[i], cudaStreamNonBlocking) != cudaSuccess)
+          return fail(MBCI_ERR_CUDA, "stream creation failed");
+      for (auto& ev : h->cev)
+        if (!ev && cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess)
+          return fail(MBCI_ERR_CUDA, "event creation failed");
+      // sub-handles first (host work, outside the capture)
+      std::vector<mbci_chain*> runs;
+      for (int64_t c = 0; c < n_chunks; ++c) {
+        const int64_t nb = std::min(cb, d.batch - c * cb);
+        if (nb <= 0) break;
+        mbci_chain* sub = nullptr;
+        for (auto& sh : h->sub)
+          if (sh && sh->d.batch == nb) sub = sh;
+        if (!sub) {
+          mbci_chain_desc_t sd = d;
+          sd.batch = nb;
+          sd.tune = 0;
+          mbci_chain_t nh = nullptr;
+          mbci_status_t rs = create_impl(&sd, h->device, &h->plan, &nh);
+          if (rs != MBCI_OK) return rs;
+          for (auto& sh : h->sub)
+            if (!sh) { sh = nh; nh = nullptr; break; }
+          if (nh) {
+            mbci_chain_destroy(nh);
+            return fail(MBCI_ERR_CUDA, "run_host: sub-handle cache full");
+          }
+          sub = h->sub[0]->d.batch == nb ? h->sub[0] : h->sub[1];
+        }
+        runs.push_back(sub);
+      }
+      cudaError_t ce = cudaStreamBeginCapture(h->cst[0], cudaStreamCaptureModeThreadLocal);
+      if (ce != cudaSuccess) return cuda_fail(ce, "run_host graph capture");
+      cudaEventRecord(h->cev[0], h->cst[0]);
+      cudaStreamWaitEvent(h->cst[1], h->cev[0], 0);
+      cudaStreamWaitEvent(h->cst[2], h->cev[0], 0);
+      mbci_status_t rs = MBCI_OK;
+      for (size_t c = 0; c < runs.size() && rs == MBCI_OK; ++c)
+        rs = enqueue(runs[c], (int64_t)c * cb, runs[c]->d.batch, h->cst[0], h->cst[1], h->cst[2], h->cev[1 + 2 * c],
+                     h->cev[2 + 2 * c]);
+      // rejoin the forked streams into the capture origin
+      cudaEventRecord(h->cev[2 * kHostChunks + 1], h->cst[1]);
+      cudaEventRecord(h->cev[2 * kHostChunks + 2], h->cst[2]);
+      cudaStreamWaitEvent(h->cst[0], h->cev[2 * kHostChunks + 1], 0);
+      cudaStreamWaitEvent(h->cst[0], h->cev[2 * kHostChunks + 2], 0);
+      cudaGraph_t g = nullptr;
+      ce = cudaStreamEndCapture(h->cst[0], &g);
+      if (rs != MBCI_OK) {
+        if (g) cudaGraphDestroy(g);
+        return rs;
+      }
+      if (ce != cudaSuccess || !g) return cuda_fail(ce, "run_host graph capture");
+      ce = cudaGraphInstantiate(&h->hg_exec, g, 0);
+      cudaGraphDestroy(g);
+      if (ce != cudaSuccess) {
+        h->hg_exec = nullptr;
+        return cuda_fail(ce, "run_host graph instantiate");
+      }
+      for (int i = 0; i < 5; ++i) h->hg_key[i] = key[i];
+    }
+    cudaError_t e = cudaGraphLaunch(h->hg_exec, ust);
+    if (e != cudaSuccess) return cuda_fail(e, "run_host graph launch");
+    e = cudaStreamSynchronize(ust);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
+    return MBCI_OK;
   }
-  mbci_status_t rs = launch(h, h->dA, h->dB, h->dD, h->dE, dv, st);
+  // pageable host memory: the serial pipeline on `stream`
+  mbci_status_t rs = enqueue(h, 0, d.batch, ust, ust, ust, nullptr, nullptr);
   if (rs != MBCI_OK) return rs;
-  // E back row by row (2-D copies) so host bytes between rows are never overwritten
-  if (d.bs_e == d.M * d.ld_e) {
-    e = cudaMemcpy2DAsync(E, d.ld_e * s, h->dE, d.ld_e * s, d.L * s, d.batch * d.M, cudaMemcpyDeviceToHost, st);
-  } else {
-    for (int64_t b = 0; b < d.batch && e == cudaSuccess; ++b)
-      e = cudaMemcpy2DAsync((char*)E + b * d.bs_e * s, d.ld_e * s, (char*)h->dE + b * d.bs_e * s, d.ld_e * s,
-                            d.L * s, d.M, cudaMemcpyDeviceToHost, st);
-  }
-  if (e != cudaSuccess) return cuda_fail(e, "D2H E");
-  e = cudaStreamSynchronize(st);
+  cudaError_t e = cudaStreamSynchronize(ust);
   if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
   return MBCI_OK;
 }
 
 mbci_status_t mbci_chain_destroy(mbci_chain_t h) {
   if (!h) return MBCI_OK;
+  for (auto& sh : h->sub) mbci_chain_destroy(sh);
+  for (auto& c : h->cst)
+    if (c) cudaStreamDestroy(c);
+  for (auto& ev : h->cev)
+    if (ev) cudaEventDestroy(ev);
+  if (h->hg_exec) cudaGraphExecDestroy(h->hg_exec);
   cudaFree(h->dA);
   cudaFree(h->dB);
   cudaFree(h->dD);
