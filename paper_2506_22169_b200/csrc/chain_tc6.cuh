@@ -66,8 +66,8 @@ __device__ __forceinline__ void t6_exp_half(uint32_t (&pk)[32], const uint32_t (
 }
 
 // NONE / SCALE: P = cvt(scale · S) for a 64-column half row
-template <bool BF16>
-__device__ __forceinline__ void t6_cvt_half(uint32_t tP, const uint32_t (&sr)[64], float sc, int op) {
+template <bool BF16, bool ACT>
+__device__ __forceinline__ void t6_cvt_half_impl(uint32_t tP, const uint32_t (&sr)[64], float sc, int op) {
   const float2 sc2 = make_float2(sc, sc);
 #pragma unroll
   for (int ch = 0; ch < 2; ++ch) {
@@ -76,7 +76,7 @@ __device__ __forceinline__ void t6_cvt_half(uint32_t tP, const uint32_t (&sr)[64
     for (int c = 0; c < 16; ++c) {
       const int cp = ch * 16 + c;
       float2 z = __fmul2_rn(make_float2(__uint_as_float(sr[2 * cp]), __uint_as_float(sr[2 * cp + 1])), sc2);
-      if (op >= 3) {
+      if constexpr (ACT) {
         z.x = ptx::act(op, z.x);
         z.y = ptx::act(op, z.y);
       }
@@ -84,6 +84,11 @@ __device__ __forceinline__ void t6_cvt_half(uint32_t tP, const uint32_t (&sr)[64
     }
     ptx::tmem_st16(tP + ch * 16, pk);
   }
+}
+template <bool BF16>
+__device__ __forceinline__ void t6_cvt_half(uint32_t tP, const uint32_t (&sr)[64], float sc, int op) {
+  if (op >= 3) t6_cvt_half_impl<BF16, true>(tP, sr, sc, op);
+  else t6_cvt_half_impl<BF16, false>(tP, sr, sc, op);
 }
 
 // Extreme (max, or min for a negative scale) of a 64-column half row; MASKED: first `valid` only.
