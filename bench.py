@@ -406,6 +406,7 @@ def run_cuda(args, rank, world, local_rank):
         "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "us_per_chain": ms_per_step * 1e3,
         "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": dtype, "data": "synthetic",
+        "mbci_env": {k: v for k, v in sorted(os.environ.items()) if k.startswith("MBCI_")},
         "config": {"workload": desc, "name": name, "batch_heads_per_gpu": nb, "global_batch_heads": global_b,
                    "M": M, "N": N, "K": K, "L": L, "op": op, "scale": sc, "b_layout": b_layout,
                    "l2": f"{rot} rotating input sets ({rot * step_bytes / 2**20:.0f} MiB) > 2x L2 between reuses",
