@@ -58,6 +58,10 @@ def lib():
                                       ctypes.c_int, ctypes.c_double, ctypes.c_int, vp, ctypes.c_int, vp, i64,
                                       ctypes.c_int, dp]
         L.oracle_chain_ex.restype = ctypes.c_int
+        L.oracle_chain3.argtypes = [vp, vp, vp, vp, dp, ctypes.c_int, i64, i64, i64, i64, i64, i64, ctypes.c_int,
+                                    ctypes.c_double, ctypes.c_int, vp, ctypes.c_int, ctypes.c_int,
+                                    ctypes.c_double, ctypes.c_int]
+        L.oracle_chain3.restype = ctypes.c_int
         L.oracle_decode_array.argtypes = [vp, ctypes.c_int, i64, dp]
         L.oracle_decode_array.restype = ctypes.c_int
         L.oracle_max_threads.restype = ctypes.c_int
@@ -116,6 +120,23 @@ def chain(inp, op: str, scale: float = 1.0, valid_len=None, rows=None,
     if rc != 0:
         raise ValueError("oracle_chain rejected its arguments")
     return (E, Cp) if want_cprime else E
+
+
+def chain3(inp, F, H: int, op: str, scale: float, op2: str, scale2: float = 1.0, valid_len=None,
+           causal: bool = False, nthreads: int = 0):
+    """fp64 E3 [batch, M, H] = op2(op(A·B)·D) · F for ``inp`` and F (storage bits [batch, L, H])."""
+    A = np.ascontiguousarray(inp.A)
+    B = np.ascontiguousarray(inp.B)
+    D = np.ascontiguousarray(inp.D)
+    Fb = np.ascontiguousarray(F)
+    vl = None if valid_len is None else np.ascontiguousarray(valid_len, dtype=np.int32)
+    E = np.empty((inp.batch, inp.M, H), dtype=np.float64)
+    rc = lib().oracle_chain3(_ptr(A), _ptr(B), _ptr(D), _ptr(Fb), _ptr(E), DTYPE_CODE[inp.dtype], inp.batch,
+                             inp.M, inp.N, inp.K, inp.L, H, OP_CODE[op], float(scale), inp.b_layout, _ptr(vl),
+                             1 if causal else 0, OP_CODE[op2], float(scale2), int(nthreads))
+    if rc != 0:
+        raise ValueError("oracle_chain3 rejected its arguments")
+    return E
 
 
 def row_max_error(E_gpu: np.ndarray, E_ref: np.ndarray) -> float:

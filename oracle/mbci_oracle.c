@@ -31,6 +31,9 @@
  *                   mu = max_n z[n]; if mu == -inf: C'[n] = 0 for all n;
  *                   else e[n] = exp(z[n]-mu), Z = sum_n e[n], C'[n] = e[n]/Z
  *   4. E[β,m,l] = sum_{n<N} C'[n] * D[β,n,l]
+ * oracle_chain3 (R20): a third contraction
+ *   5. O2[l] = op2(E[β,m,l])  (NONE, SCALE s2·x, RELU, GELU as in step 3)
+ *   6. E3[β,m,h] = sum_{l<L} O2[l] * F[β,l,h]
  */
 #include <math.h>
 #include <stdint.h>
@@ -225,6 +228,61 @@ int oracle_chain_ex(const void* A, const void* B, const void* D, double* E, int 
       }
       free(a); free(b); free(d); free(C);
     }
+  }
+  return err ? -1 : 0;
+}
+
+/* Three-contraction chain: E3 [batch, M, H] = op2(op(A·B)·D) · F, F [batch, L, H] packed row-major
+ * storage bits; op2 in {NONE, SCALE, RELU, GELU} with scale2; the rest as oracle_chain_ex.
+ * Plain and unfused: the two-contraction row of steps 1-4, then steps 5-6 per row. */
+int oracle_chain3(const void* A, const void* B, const void* D, const void* F, double* E3, int dtype,
+                  int64_t batch, int64_t M, int64_t N, int64_t K, int64_t L, int64_t H, int op,
+                  double scale, int b_layout, const int32_t* valid_len, int causal, int op2, double scale2,
+                  int nthreads) {
+  if (batch < 0 || M < 0 || N < 0 || K < 0 || L < 0 || H < 0) return -1;
+  if (dtype < 0 || dtype > 2 || op < 0 || op > 4 || b_layout < 0 || b_layout > 1) return -1;
+  if (op2 != ORC_OP_NONE && op2 != ORC_OP_SCALE && op2 != ORC_OP_RELU && op2 != ORC_OP_GELU) return -1;
+  if (op != ORC_OP_SOFTMAX) causal = 0;
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#else
+  (void)nthreads;
+#endif
+  int err = 0;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t beta = 0; beta < batch; ++beta) {
+    double* a = (double*)malloc((size_t)ORC_MAX1(M * K) * sizeof(double));
+    double* b = (double*)malloc((size_t)ORC_MAX1(K * N) * sizeof(double));
+    double* d = (double*)malloc((size_t)ORC_MAX1(N * L) * sizeof(double));
+    double* f = (double*)malloc((size_t)ORC_MAX1(L * H) * sizeof(double));
+    double* C = (double*)malloc((size_t)ORC_MAX1(N) * sizeof(double));
+    double* e = (double*)malloc((size_t)ORC_MAX1(L) * sizeof(double));
+    if (!a || !b || !d || !f || !C || !e) {
+#pragma omp atomic write
+      err = 1;
+    } else {
+      decode_span(A, dtype, beta * M * K, M * K, a);
+      decode_span(B, dtype, beta * K * N, K * N, b);
+      decode_span(D, dtype, beta * N * L, N * L, d);
+      decode_span(F, dtype, beta * L * H, L * H, f);
+      int64_t vlen = clamp_vlen(op, valid_len, beta, N);
+      for (int64_t m = 0; m < M; ++m) {
+        chain_row(a + m * K, b, d, N, K, L, op, scale, b_layout, row_limit(vlen, causal, m), C, e, NULL);
+        for (int64_t l = 0; l < L; ++l) {       /* step 5 */
+          double x = e[l];
+          if (op2 == ORC_OP_SCALE) x = scale2 * x;
+          else if (op2 == ORC_OP_RELU) x = (scale2 * x > 0.0) ? scale2 * x : 0.0;
+          else if (op2 == ORC_OP_GELU) x = 0.5 * (scale2 * x) * (1.0 + erf((scale2 * x) / sqrt(2.0)));
+          e[l] = x;
+        }
+        for (int64_t hh = 0; hh < H; ++hh) {    /* step 6 */
+          double acc = 0.0;
+          for (int64_t l = 0; l < L; ++l) acc += e[l] * f[l * H + hh];
+          E3[(beta * M + m) * H + hh] = acc;
+        }
+      }
+    }
+    free(a); free(b); free(d); free(f); free(C); free(e);
   }
   return err ? -1 : 0;
 }

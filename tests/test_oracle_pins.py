@@ -366,3 +366,43 @@ def test_chain_schedule_dead_loop_and_hoist():
     # hoisted bytes equal the algorithmic (M+N)(K+L)s per batch when every tile covers its dim
     mem, _, _ = model.chain_schedule(1, 256, 256, 64, 64, 256, 256, 64, 64, 2)
     assert sum(ts * math.prod(lp) for ts, lp in mem) == (256 + 256) * (64 + 64) * 2
+
+
+# ---------------------------------------------------------------- three contractions (R20)
+def test_chain3_identity_F_and_reassociation():
+    """oracle.chain3: F = I (H = L) gives op2 of the two-contraction chain exactly; NONE / NONE on
+    integer inputs equals the two-contraction chain with D·F (exact integer arithmetic)."""
+    inp = gen.make_chain_inputs(51, "bf16", 2, 9, 13, 7, 6, 1)
+    eye = np.broadcast_to(np.eye(6), (2, 6, 6))
+    Fi = (np.asarray(eye, np.float32).view(np.uint32) >> np.uint32(16)).astype(np.uint16)
+    E2 = oracle.chain(inp, "softmax", 0.4)
+    assert np.array_equal(oracle.chain3(inp, Fi, 6, "softmax", 0.4, "none"), E2)
+    assert np.array_equal(oracle.chain3(inp, Fi, 6, "softmax", 0.4, "relu", 1.0), np.maximum(E2, 0.0))
+    assert np.array_equal(oracle.chain3(inp, Fi, 6, "softmax", 0.4, "scale", -2.0), -2.0 * E2)
+    ii = gen.make_chain_inputs(52, "f16", 2, 5, 7, 4, 3, 0, kind="int")
+    F = gen.make_chain_inputs(53, "f16", 2, 3, 1, 5, 1, 0, kind="int").A   # [2, L=3, H=5] (A's [b, M, K] shape)
+    D = gen.bits_to_f64_numpy(ii.D, "f16")
+    DF = D @ gen.bits_to_f64_numpy(F, "f16")                          # |DF| <= 12: exact in fp16
+    ii2 = gen.ChainInputs(ii.A, ii.B, gen._f64_to_storage(DF.ravel(), "f16").reshape(2, 7, 5), None, "f16", 2, 5,
+                          7, 4, 5, 0)
+    assert np.array_equal(oracle.chain3(ii, F, 5, "none", 1.0, "none"), oracle.chain(ii2, "none", 1.0))
+
+
+def test_chain3_brute_force_numpy():
+    inp = gen.make_chain_inputs(54, "f16", 3, 6, 10, 5, 4, 1, valid_len_range=(1, 10))
+    F = gen.make_chain_inputs(55, "f16", 3, 4, 1, 7, 1, 1).A   # [3, L=4, H=7]
+    A = gen.bits_to_f64_numpy(inp.A, "f16")
+    B = gen.bits_to_f64_numpy(inp.B, "f16")
+    D = gen.bits_to_f64_numpy(inp.D, "f16")
+    Ff = gen.bits_to_f64_numpy(F, "f16")
+    from scipy.special import erf as sp_erf
+    for causal in (False, True):
+        got = oracle.chain3(inp, F, 7, "softmax", 0.3, "gelu", 1.7, valid_len=inp.valid_len, causal=causal)
+        for b in range(3):
+            for m in range(6):
+                lim = min(int(inp.valid_len[b]), m + 1) if causal else int(inp.valid_len[b])
+                z = 0.3 * (A[b, m] @ B[b, :lim].T)
+                p = np.exp(z - z.max())
+                e = (p / p.sum()) @ D[b, :lim]
+                g = 0.5 * 1.7 * e * (1.0 + sp_erf(1.7 * e / math.sqrt(2.0)))
+                assert np.max(np.abs(got[b, m] - g @ Ff[b])) < 1e-12
