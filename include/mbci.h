@@ -157,6 +157,27 @@ mbci_status_t mbci_chain_run_host(mbci_chain_t h, const void* A, const void* B, 
  * the handle ran on.  NULL is a no-op. */
 mbci_status_t mbci_chain_destroy(mbci_chain_t h);
 
+/* ---- three-contraction chains (R20) -------------------
+ * E3[b,m,h] = sum_l op2(E[b,m,l]) * F[b,l,h] with E = op(A·B)·D as above: a third contraction whose
+ * inputs never leave the chip (kernel 0: O -> P2 in tensor memory -> tcgen05.mma with F staged by
+ * TMA; H cut into chunks of <= 128 columns on the grid).  op2 in {NONE, SCALE (scale2), RELU, GELU}
+ * (activations on scale2 · x; NaN scale2 -> 1).  fp16 / bf16, packed row-major layouts only:
+ * A [b,M,K], B [b,K,N] or [b,N,K], D [b,N,L], F [b,L,H], E3 [b,M,H]; 1 <= L <= 128, K, N, L, H
+ * multiples of 8 (16-byte TMA rows).  Masks and ops of the first two contractions as mbci_chain_*.
+ * The handle is an mbci_chain_t: mbci_chain_plan / describe / destroy apply. */
+typedef struct {
+  int64_t batch, M, N, K, L, H;
+  int32_t dtype, op;
+  float scale;
+  int32_t mask, b_layout;
+  int32_t op2;
+  float scale2;
+} mbci_chain3_desc_t;
+mbci_status_t mbci_chain3_create(const mbci_chain3_desc_t* desc, int device, mbci_chain_t* out);
+/* A, B, D, F, E3: DEVICE pointers, 16-byte aligned; valid_len as mbci_chain_run.  Asynchronous. */
+mbci_status_t mbci_chain3_run(mbci_chain_t h, const void* A, const void* B, const void* D, const void* F,
+                              void* E3, const int32_t* valid_len, void* stream);
+
 /* ---- introspection ---------------------------------------------------------------------- */
 
 /* The chosen plan (copy). */

@@ -193,6 +193,9 @@ struct mbci_chain {
   int32_t search_rounds = 0, search_measurements = 0;   // tune = 2 (Algorithm 1) statistics
   Tc4Params tp4{};
   Tf32Params tp7{};          // kernel 7 (fp32, 3xTF32)
+  CUtensorMap tmF;           // chain3: F's tensor map (encoded per F pointer)
+  const void* tmF_ptr = nullptr;
+  bool chain3 = false;
   int32_t grid2 = 0;
   int32_t kch = 1, dch = 1;
   MapCacheEntry cache[16];   // tensor maps of the 16 most recent (A, B, D) pointer triples
@@ -422,7 +425,8 @@ mbci_status_t launch(mbci_chain* h, const void* A, const void* B, const void* D,
       t.valid_len = vl;
       t.E = E;
       t.trace = h->trace;
-      h->tc<<<(unsigned)h->plan.n_block, kThreads, h->plan.smem_bytes, st>>>(ent->ta, ent->tb, ent->td, t);
+      h->tc<<<(unsigned)h->plan.n_block, kThreads, h->plan.smem_bytes, st>>>(ent->ta, ent->tb, ent->td,
+                                                                          t.c3 ? h->tmF : ent->td, t);
     } else if (h->plan.kernel == 4) {
       Tc4Params t = h->tp4;
       t.valid_len = vl;
@@ -899,6 +903,113 @@ mbci_status_t mbci_chain_run_host(mbci_chain_t h, const void* A, const void* B, 
   cudaError_t e = cudaStreamSynchronize(ust);
   if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
   return MBCI_OK;
+}
+
+// ---- three-contraction chains (R20) --------------------------------
+mbci_status_t mbci_chain3_create(const mbci_chain3_desc_t* desc3, int device, mbci_chain_t* out) {
+  if (!desc3 || !out) return fail(MBCI_ERR_INVALID, "NULL argument");
+  *out = nullptr;
+  const mbci_chain3_desc_t& c = *desc3;
+  if (c.H < 0) return fail(MBCI_ERR_INVALID, "negative H");
+  if (c.op2 != MBCI_OP_NONE && c.op2 != MBCI_OP_SCALE && c.op2 != MBCI_OP_RELU && c.op2 != MBCI_OP_GELU)
+    return fail(MBCI_ERR_INVALID, "op2 must be NONE, SCALE, RELU or GELU");
+  mbci_chain_desc_t d{};
+  d.batch = c.batch; d.M = c.M; d.N = c.N; d.K = c.K; d.L = c.L;
+  d.dtype = c.dtype; d.op = c.op; d.scale = c.scale; d.mask = c.mask; d.b_layout = c.b_layout;
+  d.ld_e = c.H;
+  d.bs_e = c.M * c.H;
+  mbci_chain_desc_t n;
+  mbci_status_t s = normalize(&d, &n);
+  if (s != MBCI_OK) return s;
+  if (n.dtype == MBCI_F32) return fail(MBCI_ERR_UNSUPPORTED, "chain3 takes fp16 / bf16");
+  if (n.L < 1 || n.L > 128) return fail(MBCI_ERR_UNSUPPORTED, "chain3 keeps the intermediate on chip: 1 <= L <= 128");
+  if (!tc_eligible(n) || c.H % 8 != 0) return fail(MBCI_ERR_UNSUPPORTED, "chain3 needs 16-byte rows (K, N, L, H % 8)");
+  s = check_device(device);
+  if (s != MBCI_OK) return s;
+  DeviceGuard guard(device);
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return fail(MBCI_ERR_CUDA, "device properties");
+  const int32_t k_steps = static_cast<int32_t>((n.K + 15) / 16);
+  const int32_t lpad = static_cast<int32_t>(std::max<int64_t>(16, (n.L + 15) / 16 * 16));
+  // plan: kernel 0, the whole L per CTA (TL = L padded), H in TH-column chunks on the grid
+  mbci_plan_t best{};
+  bool found = false;
+  for (int32_t BN : {128, 64}) {
+    for (int32_t TH : {128, 64}) {
+      if (TH > 64 && c.H <= 64) continue;
+      const int32_t cols = 2 * BN + lpad + TH;
+      if (cols > 512) continue;
+      for (int32_t st = 4; st >= 2 && !found; --st) {
+        const int64_t f_bytes = (int64_t)(TH / 64) * lpad * 128;
+        const int64_t smem = tc_smem_bytes(k_steps, BN, lpad, st, n.b_layout, nullptr, nullptr, nullptr) + 1024 + f_bytes;
+        if (smem > prop.sharedMemPerBlockOptin) continue;
+        best = mbci_plan_t{};
+        best.kernel = 0; best.BM = 128; best.BN = BN; best.TK = 16 * std::max(1, k_steps); best.TL = lpad;
+        best.stages = st; best.smem_bytes = (int32_t)smem; best.tmem_cols = cols;
+        found = true;
+      }
+      if (found) {
+        mbci_chain* h = new (std::nothrow) mbci_chain();
+        if (!h) return fail(MBCI_ERR_NOMEM, "handle allocation failed");
+        h->d = n;
+        h->device = device;
+        h->plan = best;
+        h->chain3 = true;
+        s = setup_plan(h);
+        if (s != MBCI_OK) {
+          delete h;
+          return s;
+        }
+        TcParams& t = h->tp;
+        t.c3 = 1;
+        t.H = (int32_t)c.H;
+        t.TH = TH;
+        t.op2 = c.op2;
+        t.scale2 = c.op2 == MBCI_OP_NONE ? 1.0f : (std::isnan(c.scale2) ? 1.0f : c.scale2);
+        t.f_bytes = (uint32_t)((TH / 64) * lpad * 128);
+        t.idesc3 = ptx::idesc_f16(n.dtype == MBCI_BF16 ? 1u : 0u, 0, 1u, 128, (uint32_t)TH);
+        t.l_h = (int32_t)((c.H + TH - 1) / TH);
+        int32_t tc = 32;
+        while (tc < 2 * BN + lpad + TH) tc <<= 1;
+        t.tmem_cols = (uint32_t)tc;
+        h->plan.tmem_cols = tc;
+        h->plan.smem_bytes = best.smem_bytes;
+        h->plan.n_block = n.batch * t.l_m * t.l_h;
+        if (h->plan.n_block > INT32_MAX) {
+          delete h;
+          return fail(MBCI_ERR_UNSUPPORTED, "chain3 grid exceeds 2^31 - 1 CTAs");
+        }
+        cudaError_t e = cudaFuncSetAttribute((const void*)h->tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             h->plan.smem_bytes);
+        if (e != cudaSuccess) {
+          delete h;
+          return cuda_fail(e, "cudaFuncSetAttribute");
+        }
+        *out = h;
+        return MBCI_OK;
+      }
+    }
+  }
+  return fail(MBCI_ERR_UNSUPPORTED, "chain3: no plan fits shared / tensor memory");
+}
+
+mbci_status_t mbci_chain3_run(mbci_chain_t h, const void* A, const void* B, const void* D, const void* F, void* E,
+                              const int32_t* valid_len, void* stream) {
+  if (!h || !h->chain3) return fail(MBCI_ERR_INVALID, "not a chain3 handle");
+  const mbci_chain_desc_t& d = h->d;
+  if (d.batch == 0 || d.M == 0 || h->tp.H == 0) return MBCI_OK;
+  if (d.N > 0 && !F) return fail(MBCI_ERR_INVALID, "F is NULL");
+  if (F && !aligned16(F)) return fail(MBCI_ERR_UNSUPPORTED, "F must be 16-byte aligned");
+  DeviceGuard guard(h->device);
+  if (d.N > 0 && F != h->tmF_ptr) {
+    mbci_status_t s = get_encoder();
+    if (s != MBCI_OK) return s;
+    s = encode3d(&h->tmF, F, d.dtype == MBCI_BF16, h->tp.H, d.L, d.batch, h->tp.H, d.L * h->tp.H,
+                 (uint32_t)h->tp.TL);
+    if (s != MBCI_OK) return s;
+    h->tmF_ptr = F;
+  }
+  return launch(h, A, B, D, E, valid_len, reinterpret_cast<cudaStream_t>(stream));
 }
 
 mbci_status_t mbci_chain_destroy(mbci_chain_t h) {

@@ -50,6 +50,15 @@ struct TcParams {
   uint32_t tmem_cols;
   uint32_t idesc1, idesc2;
   uint64_t* trace;   // optional per-CTA event timestamps (debug; see mbci_chain_set_trace)
+  // Third contraction (mbci_chain3): E = op2(scale2 · O') · F with O' = op(A·B)·D
+  // (softmax-normalised).  The CTA keeps the whole L (TL = L padded, one h chunk for D) and the grid's
+  // h index walks H in chunks of TH columns; O' -> P2 (16-bit, TMEM) -> G3 (TS MMA, F from SMEM).
+  int32_t c3;        // 0: two-GEMM chain
+  int32_t H, TH;
+  int32_t op2;       // 0 none, 1 scale, 3 relu, 4 gelu
+  float scale2;
+  uint32_t f_bytes;  // F tile (L rows x TH columns) in SMEM
+  uint32_t idesc3;
 };
 
 // Trace slots (kTraceSlots x u64 per CTA, globaltimer ns unless noted).
@@ -69,7 +78,8 @@ constexpr float kRescaleTau = 8.0f;   // lazy rescale threshold, log2 units (P <
 template <bool BF16, int BN, int KCH, int BL, int DCH>
 __global__ void __launch_bounds__(kThreads, BN == 64 ? 2 : 1)
     k_chain_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-               const __grid_constant__ CUtensorMap tmD, const TcParams p) {
+               const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmF,
+               const TcParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -87,7 +97,11 @@ __global__ void __launch_bounds__(kThreads, BN == 64 ? 2 : 1)
   uint64_t* p_full = s_full + 2;    // [2]
   uint64_t* o_done = p_full + 2;    // [1] one completion per G2(i)
   uint64_t* o_final = o_done + 1;   // [1] one completion after the last G2
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_final + 1);
+  uint64_t* p2_full = o_final + 1;  // [1] chain3: row warps wrote P2 (128 arrivals)
+  uint64_t* f_full = p2_full + 1;   // [1] chain3: F tile landed
+  uint64_t* e3_full = f_full + 1;   // [1] chain3: G3 completed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(e3_full + 1);
+  uint8_t* sF = reinterpret_cast<uint8_t*>(bars) + 1024;   // chain3: F tile after the barrier block
 
   const int warp = threadIdx.x >> 5;
   const int unit = blockIdx.x;
@@ -102,7 +116,8 @@ __global__ void __launch_bounds__(kThreads, BN == 64 ? 2 : 1)
   const int mt = (unit / p.l_h) % p.l_m;
   const int beta = unit / (p.l_h * p.l_m);
   const int m0 = mt * 128;
-  const int h0 = ht * p.TL;
+  const int h0 = p.c3 ? 0 : ht * p.TL;    // D / O columns of this CTA (chain3: the whole L)
+  const int h3 = ht * p.TH;                // chain3: F / E columns of this CTA
 
   int n_lim = p.N;
   if (p.op == 2 && p.valid_len != nullptr) n_lim = min(max(p.valid_len[beta], 0), p.N);
@@ -125,7 +140,11 @@ __global__ void __launch_bounds__(kThreads, BN == 64 ? 2 : 1)
     }
     ptx::mbar_init(o_done, 1);
     ptx::mbar_init(o_final, 1);
+    ptx::mbar_init(p2_full, kRowThreads);
+    ptx::mbar_init(f_full, 1);
+    ptx::mbar_init(e3_full, 1);
     ptx::fence_mbar_init();
+    if (p.c3 && nt > 0) ptx::tma_prefetch(&tmF);
     if (nt > 0) {  // maps are only encoded when the operands exist
       if (p.k_steps > 0) {
         ptx::tma_prefetch(&tmA);
@@ -183,8 +202,14 @@ __global__ void __launch_bounds__(kThreads, BN == 64 ? 2 : 1)
       }
     }
   } else if (warp == 6) {
-    // ------------------------------------------------------------ TMA producer: D_j
-    if (ptx::elect_one() && nt > 0) {
+    // ------------------------------------------------------------ TMA producer: D_j (and F)
+    const bool elected6 = ptx::elect_one();
+    if (elected6 && nt > 0 && p.c3) {   // chain3: the F tile once, up front
+      ptx::mbar_arrive_expect_tx(f_full, p.f_bytes);
+      for (int c = 0; c < p.TH / 64; ++c)
+        ptx::tma_load_3d(sF + c * (p.TL * 128), &tmF, f_full, h3 + c * 64, 0, beta);
+    }
+    if (elected6 && nt > 0) {
       for (int j = 0; j < nt; ++j) {
         const int s = j % S;
         if (j >= S) ptx::mbar_wait(&d_empty[s], ((j / S) - 1) & 1);
@@ -261,6 +286,18 @@ __global__ void __launch_bounds__(kThreads, BN == 64 ? 2 : 1)
           ptx::mma_commit(o_done);
           if (i == nt - 1) ptx::mma_commit(o_final);
         }
+      }
+      if (p.c3) {   // G3: E3 = P2 · F_h (P2 from TMEM columns [0, TL/2) of S_0, F MN-major in SMEM)
+        ptx::mbar_wait(p2_full, 0);
+        ptx::mbar_wait(f_full, 0);
+        ptx::tc_fence_after();
+        const uint32_t tE3 = tmem + 2 * BN + p.TL;
+        const uint32_t f_base = ptx::smem_u32(sF);
+        for (int ks = 0; ks < p.TL / 16; ++ks) {
+          const uint64_t fd = ptx::sdesc_sw128(f_base + ks * 2048, p.TL * 128, 1024);
+          ptx::mma_ts(tE3, tmem + ks * 8, fd, p.idesc3, ks > 0 ? 1u : 0u);
+        }
+        ptx::mma_commit(e3_full);
       }
     }
   } else {
@@ -397,16 +434,47 @@ __global__ void __launch_bounds__(kThreads, BN == 64 ? 2 : 1)
       ptx::tc_fence_after();
     }
     if (tr && threadIdx.x == 0) tr[kTrEpi] = ptx::globaltimer();
-    const float inv = (p.op == 2) ? (l_run > 0.f ? 1.0f / l_run : 0.f) : 1.0f;
+    float inv = (p.op == 2) ? (l_run > 0.f ? 1.0f / l_run : 0.f) : 1.0f;
     const int gm = m0 + row;
-    const int ncols = min(TLP, p.L - h0);
+    uint32_t tOut = tO;
+    int outc = TLP, ncols = min(TLP, p.L - h0), ecol0 = h0;
+    if (p.c3) {
+      // P2 = cvt(op2(scale2 · O / l)) into TMEM columns [0, TL/2) of S_0 (every G2 has completed)
+      if (nt > 0) {
+        for (int c0 = 0; c0 < TLP; c0 += 32) {
+          uint32_t r[32], pk2[16];
+          ptx::tmem_ld32(tO + c0, r);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            float v0 = __uint_as_float(r[2 * q]) * inv, v1 = __uint_as_float(r[2 * q + 1]) * inv;
+            if (p.op2 != 0) {
+              v0 = ptx::act(p.op2, p.scale2 * v0);
+              v1 = ptx::act(p.op2, p.scale2 * v1);
+            }
+            pk2[q] = ptx::pack2<BF16>(v0, v1);
+          }
+          ptx::tmem_st16(tS + c0 / 2, pk2);
+        }
+        ptx::tmem_wait_st();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(p2_full);
+        ptx::mbar_wait(e3_full, 0);
+        ptx::tc_fence_after();
+      }
+      tOut = tmem + lane_off + 2 * BN + p.TL;
+      outc = p.TH;
+      ncols = min(p.TH, p.H - h3);
+      ecol0 = h3;
+      inv = 1.0f;
+    }
     using T16 = uint16_t;
     T16* erow = reinterpret_cast<T16*>(p.E) + static_cast<int64_t>(beta) * p.bs_e +
-                static_cast<int64_t>(gm) * p.ld_e + h0;
-    for (int c0 = 0; c0 < TLP; c0 += 16) {
+                static_cast<int64_t>(gm) * p.ld_e + ecol0;
+    for (int c0 = 0; c0 < outc; c0 += 16) {
       uint32_t r[16];
       if (nt > 0) {
-        ptx::tmem_ld16(tO + c0, r);
+        ptx::tmem_ld16(tOut + c0, r);
         ptx::tmem_wait_ld();
       } else {
 #pragma unroll

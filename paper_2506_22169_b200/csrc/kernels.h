@@ -12,7 +12,7 @@
 
 namespace mbci {
 
-using TcKernel = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, TcParams);
+using TcKernel = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, TcParams);
 using Tc4Kernel = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, Tc4Params);
 using Tc5Kernel = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, Tc4Params);
 

@@ -94,6 +94,16 @@ class mbci_search_result_t(ctypes.Structure):
                 ("best_measured", ctypes.c_double), ("history_min", ctypes.c_double)]
 
 
+class mbci_chain3_desc_t(ctypes.Structure):
+    _fields_ = [("batch", ctypes.c_int64), ("M", ctypes.c_int64), ("N", ctypes.c_int64), ("K", ctypes.c_int64),
+                ("L", ctypes.c_int64), ("H", ctypes.c_int64), ("dtype", ctypes.c_int32), ("op", ctypes.c_int32),
+                ("scale", ctypes.c_float), ("mask", ctypes.c_int32), ("b_layout", ctypes.c_int32),
+                ("op2", ctypes.c_int32), ("scale2", ctypes.c_float)]
+
+
+_lib.mbci_chain3_create.argtypes = [_P(mbci_chain3_desc_t), ctypes.c_int, _P(_vp)]
+_lib.mbci_chain3_run.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
+
 mbci_measure_fn = ctypes.CFUNCTYPE(ctypes.c_double, _P(mbci_plan_t), _vp)
 _lib.mbci_plan_search.argtypes = [_P(mbci_chain_desc_t), _P(mbci_hw_t), _P(mbci_search_params_t), mbci_measure_fn,
                                   _vp, _P(mbci_plan_t), _P(mbci_search_result_t), _P(ctypes.c_double)]
@@ -101,7 +111,8 @@ _lib.mbci_chain_search_stats.argtypes = [_vp, _P(ctypes.c_int32), _P(ctypes.c_in
 for _f in ("mbci_chain_create", "mbci_chain_create_with_plan", "mbci_chain_run", "mbci_chain_run_host",
            "mbci_chain_set_trace",
            "mbci_chain_destroy", "mbci_chain_plan", "mbci_chain_describe", "mbci_plan_enumerate",
-           "mbci_plan_select", "mbci_model_terms", "mbci_plan_search", "mbci_chain_search_stats"):
+           "mbci_plan_select", "mbci_model_terms", "mbci_plan_search", "mbci_chain_search_stats",
+           "mbci_chain3_create", "mbci_chain3_run"):
     getattr(_lib, _f).restype = _st
 
 EXPORTED = ["mbci_chain_create", "mbci_chain_create_with_plan", "mbci_chain_run", "mbci_chain_run_host",
@@ -109,7 +120,7 @@ EXPORTED = ["mbci_chain_create", "mbci_chain_create_with_plan", "mbci_chain_run"
             "mbci_chain_set_trace",
             "mbci_status_string", "mbci_last_error", "mbci_abi_version", "mbci_hw_default",
             "mbci_plan_enumerate", "mbci_plan_select", "mbci_model_terms", "mbci_plan_search",
-            "mbci_chain_search_stats"]
+            "mbci_chain_search_stats", "mbci_chain3_create", "mbci_chain3_run"]
 
 # ---- same names as the C ABI ---------------------------------------------------------------
 mbci_chain_create = _lib.mbci_chain_create
@@ -130,6 +141,8 @@ mbci_plan_select = _lib.mbci_plan_select
 mbci_model_terms = _lib.mbci_model_terms
 mbci_plan_search = _lib.mbci_plan_search
 mbci_chain_search_stats = _lib.mbci_chain_search_stats
+mbci_chain3_create = _lib.mbci_chain3_create
+mbci_chain3_run = _lib.mbci_chain3_run
 
 
 def plan_search(desc, measure, hw=None, N=512, n=8, eps=0.01, seed=1, max_rounds=64, model=0):
@@ -274,3 +287,46 @@ class Chain:
 
 def default_scale(K: int) -> float:
     return 1.0 / math.sqrt(K) if K > 0 else 1.0
+
+
+class Chain3:
+    """Three-contraction chain E3 = op2(op(A·B)·D)·F (mbci_chain3_*); torch tensors on the device."""
+
+    def __init__(self, batch, M, N, K, L, H, dtype="bf16", op="softmax", scale=float("nan"), op2="none",
+                 scale2=float("nan"), mask=False, causal=False, b_layout=1, device=0):
+        d = mbci_chain3_desc_t()
+        d.batch, d.M, d.N, d.K, d.L, d.H = batch, M, N, K, L, H
+        d.dtype = DTYPES[dtype]
+        d.op = OPS[op]
+        d.scale = scale
+        d.mask = (MBCI_MASK_KEY_PADDING if mask else 0) | (MBCI_MASK_CAUSAL if causal else 0)
+        d.b_layout = b_layout
+        d.op2 = OPS[op2]
+        d.scale2 = scale2
+        self.desc = d
+        h = _vp()
+        check(mbci_chain3_create(ctypes.byref(d), device, ctypes.byref(h)), "mbci_chain3_create")
+        self.h = h
+
+    def run(self, A, B, D, F, E, valid_len=None, stream=None):
+        import torch
+        st = (stream or torch.cuda.current_stream()).cuda_stream
+        vl = None if valid_len is None else valid_len.data_ptr()
+        check(mbci_chain3_run(self.h, A.data_ptr(), B.data_ptr(), D.data_ptr(), F.data_ptr(), E.data_ptr(), vl, st),
+              "mbci_chain3_run")
+
+    def plan(self):
+        p = mbci_plan_t()
+        check(mbci_chain_plan(self.h, ctypes.byref(p)), "mbci_chain_plan")
+        return p
+
+    def close(self):
+        if getattr(self, "h", None):
+            mbci_chain_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
