@@ -274,6 +274,10 @@ __global__ void __launch_bounds__(kT5Threads, 1)
     auto wait1 = [&](uint64_t* bar, uint32_t parity) {
       if (spin) ptx::mbar_spin(bar, parity); else ptx::mbar_wait(bar, parity);
     };
+    // flags bit 7: the TMA producer sleeps in its waits (suspend-time hint) to free issue slots
+    auto wait_tma = [&](uint64_t* bar, uint32_t parity) {
+      if (p.flags & 128) ptx::mbar_wait_lazy(bar, parity); else wait1(bar, parity);
+    };
     if (warp == 13) {
       // ============================================================ TMA producer
       if (ptx::elect_one()) {
@@ -286,7 +290,7 @@ __global__ void __launch_bounds__(kT5Threads, 1)
           const int nt = it.tiles(t4_unit_nlim(p, it.u));
           if (nt == 0) continue;
           const int qb = ai % p.q_bufs;
-          if (ai >= p.q_bufs) wait1(&q_empty[qb], ((ai / p.q_bufs) - 1) & 1);
+          if (ai >= p.q_bufs) wait_tma(&q_empty[qb], ((ai / p.q_bufs) - 1) & 1);
           if (ai > 0 || pre_entries == 0) load_q(qb, m0, beta, it.half < 0 && m0 + 128 < p.M);
           ++ai;
           for (int j = 0; j < nt; ++j) {
@@ -294,7 +298,7 @@ __global__ void __launch_bounds__(kT5Threads, 1)
               if (g < pre_entries) continue;
               const int tile = j + x * nt;   // half item: slot 1 takes tiles [nt, 2 nt)
               const int s = g % S;
-              if (g >= S) wait1(&kv_empty[s], ((g / S) - 1) & 1);
+              if (g >= S) wait_tma(&kv_empty[s], ((g / S) - 1) & 1);
               else if (g == pre_entries && pre_entries > 0) wait1(&kv_full[pre_entries - 1], 0);   // first step landed
               if (tr && g < kT4TrTiles) tr[460 + g] = t4_clk();
               load_entry(s, tile, beta);
@@ -389,6 +393,10 @@ __global__ void __launch_bounds__(kT5Threads, 1)
   } else if (warp >= 8) {
     // ============================================================ epilogue (warps 8-11)
     ptx::setmaxnreg_dec<80>();
+    // flags bit 7: the epilogue sleeps in its waits (suspend-time hint) to free issue slots
+    auto wait_epi = [&](uint64_t* bar, uint32_t parity) {
+      if (p.flags & 128) ptx::mbar_wait_lazy(bar, parity); else ptx::mbar_wait(bar, parity);
+    };
     const int row = threadIdx.x - 256;   // TMEM lane (warp 8+w reads lanes 32w..32w+31)
     const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
     const bool leader = threadIdx.x == 256;
@@ -460,8 +468,8 @@ __global__ void __launch_bounds__(kT5Threads, 1)
         float l[2], m[2];
 #pragma unroll
         for (int x = 0; x < 2; ++x) {
-          ptx::mbar_wait(&o_full[x], ai & 1);
-          ptx::mbar_wait(&l_full[x], ai & 1);
+          wait_epi(&o_full[x], ai & 1);
+          wait_epi(&l_full[x], ai & 1);
           l[x] = l_sm[x][ai & 1][row];
           m[x] = m_sm[x][ai & 1][row];
           ptx::mbar_arrive(&l_free[x]);
@@ -483,10 +491,10 @@ __global__ void __launch_bounds__(kT5Threads, 1)
       for (int x = 0; x < 2; ++x) {
         float l = 0.f;
         if (nt > 0) {
-          ptx::mbar_wait(&o_full[x], ai & 1);
+          wait_epi(&o_full[x], ai & 1);
           ptx::tc_fence_after();
           if (tr && x == 0 && row == 0 && ai < 4) tr[490 + 4 * ai] = t4_clk();
-          ptx::mbar_wait(&l_full[x], ai & 1);
+          wait_epi(&l_full[x], ai & 1);
           l = l_sm[x][ai & 1][row];
           ptx::mbar_arrive(&l_free[x]);
         }

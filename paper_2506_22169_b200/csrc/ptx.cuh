@@ -100,6 +100,28 @@ __device__ __forceinline__ void mbar_spin(uint64_t* bar, uint32_t parity) {
 
 // Wait for the phase with the given parity to complete.  A pipeline bug must not hang the
 // GPU: after ~4 s of waiting the kernel traps (the launch then reports an error).
+// try_wait with a suspend-time hint (ns): the thread may sleep up to `hint_ns` unless the phase
+// completes first — for latency-insensitive waiters (epilogue, TMA producer), so their polling
+// takes fewer issue slots from the softmax warps sharing their SMSP.
+__device__ __forceinline__ bool mbar_try_wait_hint(uint32_t addr, uint32_t parity, uint32_t hint_ns) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, P;\n\t}"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity), "r"(hint_ns)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_lazy(uint64_t* bar, uint32_t parity, uint32_t hint_ns = 20000) {
+  const uint32_t addr = smem_u32(bar);
+  if (mbar_try_wait_hint(addr, parity, hint_ns)) return;
+  const uint64_t t0 = globaltimer();
+  while (!mbar_try_wait_hint(addr, parity, hint_ns)) {
+    if (globaltimer() - t0 > 4000000000ull) __trap();
+  }
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
   if (mbar_try_wait(addr, parity)) return;

@@ -12,7 +12,11 @@ import math
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmbci_trace.so" if os.environ.get("MBCI_LIB") == "trace" else "libmbci.so")
+# MBCI_LIB: unset -> libmbci.so; "trace" -> libmbci_trace.so (diagnostics build); "ab:<name>" -> an
+# A/B copy <name> next to libmbci.so (tools only; bench.py echoes MBCI_* in its JSON line)
+_lib_sel = os.environ.get("MBCI_LIB", "")
+LIB_PATH = os.path.join(HERE, "libmbci_trace.so" if _lib_sel == "trace"
+                        else (_lib_sel[3:] if _lib_sel.startswith("ab:") else "libmbci.so"))
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
