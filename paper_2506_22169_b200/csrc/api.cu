@@ -335,8 +335,9 @@ mbci_status_t setup_plan(mbci_chain* h) {
     if (e != cudaSuccess) return cuda_fail(e, "occupancy query");
     if (occ < 1) return fail(MBCI_ERR_UNSUPPORTED, "kernel-%d CTA does not fit on an SM", p.kernel);
   } else if (p.kernel == 7) {
-    if (d.dtype != MBCI_F32 || d.K < 1 || d.K > 64 || d.L > 64 || d.N < 1)
-      return fail(MBCI_ERR_UNSUPPORTED, "kernel-7 plan needs fp32, 1 <= K <= 64, L <= 64, N >= 1");
+    if (d.dtype != MBCI_F32 || d.K < 1 || d.K > 128 || d.L > 128 || d.N < 1)
+      return fail(MBCI_ERR_UNSUPPORTED, "kernel-7 plan needs fp32, 1 <= K <= 128, L <= 128, N >= 1");
+    const bool wide = d.K > 64 || d.L > 64;   // 32-key tiles, 128 O columns (chain_tf32.cuh TfWide)
     Tf32Params& t = h->tp7;
     t = Tf32Params{};
     t.M = (int32_t)d.M; t.N = (int32_t)d.N; t.K = (int32_t)d.K; t.L = (int32_t)d.L;
@@ -348,12 +349,13 @@ mbci_status_t setup_plan(mbci_chain* h) {
     t.b_layout = d.b_layout;
     t.ld_a = d.ld_a; t.ld_b = d.ld_b; t.ld_d = d.ld_d; t.ld_e = d.ld_e;
     t.bs_a = d.bs_a; t.bs_b = d.bs_b; t.bs_d = d.bs_d; t.bs_e = d.bs_e;
-    t.idesc1 = ptx::idesc_f16(2u, 0u, 0u, 128, 64);           // kind::tf32: a/b format 2, K-major
+    t.idesc1 = ptx::idesc_f16(2u, 0u, 0u, 128, wide ? 32u : 64u);   // kind::tf32: a/b format 2, K-major
     t.idesc2 = ptx::idesc_f16(2u, 0u, 0u, 128, (uint32_t)t.TLP);
     p.n_block = d.batch * ((d.M + 127) / 128);
     if (p.n_block > INT32_MAX) return fail(MBCI_ERR_UNSUPPORTED, "kernel-7 grid exceeds 2^31 - 1 CTAs");
-    p.smem_bytes = (int32_t)kTf32Smem;
-    cudaError_t e = cudaFuncSetAttribute(tf32_fn(), cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_bytes);
+    p.smem_bytes = (int32_t)(wide ? kTf32WideSmem : kTf32Smem);
+    p.BN = wide ? 32 : 64;
+    cudaError_t e = cudaFuncSetAttribute(tf32_fn(wide), cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_bytes);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
   } else {
     if (d.batch * d.M > INT32_MAX) return fail(MBCI_ERR_UNSUPPORTED, "batch * M exceeds the CUDA-core grid");
@@ -454,8 +456,8 @@ mbci_status_t launch(mbci_chain* h, const void* A, const void* B, const void* D,
   } else if (h->plan.kernel == 7) {
     Tf32Params t = h->tp7;
     t.valid_len = vl;
-    cudaError_t le = launch_tf32((unsigned)h->plan.n_block, st, (const float*)A, (const float*)B, (const float*)D,
-                                 (float*)E, t);
+    cudaError_t le = launch_tf32(h->plan.BN == 32, (unsigned)h->plan.n_block, st, (const float*)A, (const float*)B,
+                                 (const float*)D, (float*)E, t);
     if (le != cudaSuccess) return cuda_fail(le, "kernel-7 launch");
   } else {
     SimtParams sp{};

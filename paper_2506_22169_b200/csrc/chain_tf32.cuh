@@ -30,8 +30,8 @@ namespace mbci {
 
 struct Tf32Params {
   int32_t M, N, K, L;
-  int32_t KP;    // K padded to a multiple of 8 (the TF32 MMA K step), <= 64
-  int32_t TLP;   // L padded to a multiple of 16 (the MMA N granularity), <= 64
+  int32_t KP;    // K padded to a multiple of 8 (the TF32 MMA K step), <= 64 (<= 128 for the wide variant)
+  int32_t TLP;   // L padded to a multiple of 16 (the MMA N granularity), <= 64 (<= 128)
   int32_t op;    // 0 none, 1 scale, 2 softmax, 3 relu, 4 gelu
   int32_t causal; // softmax: key n visible to row m only if n <= m (R18)
   float scale;   // softmax: scale * log2(e); SCALE: the multiplier
@@ -43,12 +43,22 @@ struct Tf32Params {
 };
 
 constexpr int kTf32Threads = 128;
-constexpr int kTf32BN = 64;                 // keys per tile
-constexpr uint32_t kTf32SCol = 0, kTf32PHiCol = 64, kTf32PLoCol = 128, kTf32OCol = 192;
-// shared memory (1024-B aligned): A_hi, A_lo [2 chunks][128 rows][128 B]; B_hi, B_lo [2][64][128 B];
-// D_hi, D_lo [2 chunks of 32 keys][64 rows (l)][128 B]
-constexpr uint32_t kTf32ABytes = 2 * 128 * 128, kTf32BBytes = 2 * 64 * 128, kTf32DBytes = 2 * 64 * 128;
-constexpr uint32_t kTf32Smem = 2 * (kTf32ABytes + kTf32BBytes + kTf32DBytes) + 1024;
+// Two instantiations (TfCfg<BN, OC>): BN keys per tile, OC = max O columns (= max K and L):
+//   <64, 64>  K, L <= 64:  A, B, D hi/lo = 2 x (32 + 16 + 16) KB;  TMEM S | P_hi | P_lo | O = 4 x 64
+//   <32, 128> K, L <= 128: A, B, D hi/lo = 2 x (64 + 16 + 16) KB;  TMEM 3 x 32 + 128
+template <int BN_, int OC_>
+struct TfCfg {
+  static constexpr int BN = BN_, OC = OC_;
+  static constexpr uint32_t A_BYTES = (OC / 32) * 128 * 128;   // K chunks of 32 fp32 x 128 rows x 128 B
+  static constexpr uint32_t B_BYTES = (OC / 32) * BN * 128;    // K chunks x BN rows
+  static constexpr uint32_t D_BYTES = (BN / 32) * OC * 128;    // key chunks x OC rows (l)
+  static constexpr uint32_t SMEM = 2 * (A_BYTES + B_BYTES + D_BYTES) + 1024;
+  static constexpr uint32_t S_COL = 0, PHI_COL = BN, PLO_COL = 2 * BN, O_COL = 3 * BN;
+};
+using TfSmall = TfCfg<64, 64>;
+using TfWide = TfCfg<32, 128>;
+constexpr uint32_t kTf32Smem = TfSmall::SMEM;      // the K, L <= 64 variant
+constexpr uint32_t kTf32WideSmem = TfWide::SMEM;   // the K, L <= 128 variant
 
 __device__ __forceinline__ void mma_ss_tf32(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                             uint32_t accumulate) {
@@ -118,9 +128,14 @@ __device__ __forceinline__ void tf32_load_split(uint8_t* dhi, uint8_t* dlo, int 
 
 // The kernel itself is compiled in k_tf32.cu only (other translation units see the parameters).
 #ifdef MBCI_TF32_KERNEL
+template <class CFG>
 __global__ void __launch_bounds__(kTf32Threads, 1)
     k_chain_tf32(const float* __restrict__ A, const float* __restrict__ B, const float* __restrict__ D,
                  float* __restrict__ E, const Tf32Params p) {
+  constexpr int kTf32BN = CFG::BN, kOC = CFG::OC;
+  constexpr uint32_t kTf32ABytes = CFG::A_BYTES, kTf32BBytes = CFG::B_BYTES, kTf32DBytes = CFG::D_BYTES;
+  constexpr uint32_t kTf32SCol = CFG::S_COL, kTf32PHiCol = CFG::PHI_COL, kTf32PLoCol = CFG::PLO_COL,
+                     kTf32OCol = CFG::O_COL;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -139,7 +154,7 @@ __global__ void __launch_bounds__(kTf32Threads, 1)
   const int warp = threadIdx.x >> 5;
   const int row = threadIdx.x;   // TMEM lane / output row m0 + row
   const bool leader = threadIdx.x == 0;
-  if (warp == 0) ptx::tmem_alloc(&tmem_base_slot, 256);
+  if (warp == 0) ptx::tmem_alloc(&tmem_base_slot, 256);   // 4 x 64 or 3 x 32 + 128 columns
   if (leader) {
     ptx::mbar_init(&mma_bar, 1);
     ptx::fence_mbar_init();
@@ -171,9 +186,9 @@ __global__ void __launch_bounds__(kTf32Threads, 1)
   // tile's 24 products per element into TMEM (acc = 0 at each tile's first MMA), which keeps its
   // non-IEEE accumulation error at the tile scale (measured: a 1000-key chain accumulated in TMEM
   // missed 1e-5 by 2 %)
-  float o[64];
+  float o[kOC];
 #pragma unroll
-  for (int c = 0; c < 64; ++c) o[c] = 0.f;
+  for (int c = 0; c < kOC; ++c) o[c] = 0.f;
   uint32_t phase = 0;
   for (int j = 0; j < ntiles; ++j) {
     const int n0 = j * kTf32BN;
@@ -184,7 +199,7 @@ __global__ void __launch_bounds__(kTf32Threads, 1)
                       1, false);
     else                   // B stored [K, N]: element (key, k) at k * ld_b + key
       tf32_load_split(sBhi, sBlo, kTf32BN, p.KP, bsrc + n0, p.N - n0, p.K, 1, p.ld_b, true);
-    tf32_load_split(sDhi, sDlo, 64, kTf32BN, D + beta * p.bs_d + static_cast<int64_t>(n0) * p.ld_d, p.L,
+    tf32_load_split(sDhi, sDlo, kOC, kTf32BN, D + beta * p.bs_d + static_cast<int64_t>(n0) * p.ld_d, p.L,
                     p.N - n0, 1, p.ld_d, true);
     ptx::fence_proxy_async_smem();
     ptx::tc_fence_before();
@@ -206,8 +221,8 @@ __global__ void __launch_bounds__(kTf32Threads, 1)
     ptx::tc_fence_after();
     // inter-GEMM op on row `row`, 64 keys
     uint32_t s[kTf32BN];
-    ptx::tmem_ld32(tS, &s[0]);
-    ptx::tmem_ld32(tS + 32, &s[32]);
+#pragma unroll
+    for (int c = 0; c < kTf32BN; c += 32) ptx::tmem_ld32(tS + c, &s[c]);
     ptx::tmem_wait_ld();
     float pv[kTf32BN];
     if (p.op == 2) {
@@ -221,7 +236,7 @@ __global__ void __launch_bounds__(kTf32Threads, 1)
         const float alpha = ptx::ex2(m_run - m_new);
         l_run *= alpha;
 #pragma unroll
-        for (int c = 0; c < 64; ++c) o[c] *= alpha;
+        for (int c = 0; c < kOC; ++c) o[c] *= alpha;
       }
       m_run = m_new;
       float sum = 0.f;
@@ -257,7 +272,7 @@ __global__ void __launch_bounds__(kTf32Threads, 1)
     // GEMM2: O += P·D_j with 3xTF32 (P from TMEM)
     if (leader) {
       for (int ks = 0; ks < kTf32BN / 8; ++ks) {
-        const uint64_t bo = static_cast<uint64_t>((ks >> 2) * (64 * 128 / 16) + (ks & 3) * 2);
+        const uint64_t bo = static_cast<uint64_t>((ks >> 2) * (kOC * 128 / 16) + (ks & 3) * 2);
         const uint32_t acc = ks > 0 ? 1u : 0u;
         mma_ts_tf32(tmem + kTf32OCol, tmem + kTf32PHiCol + ks * 8, dDhi + bo, p.idesc2, acc);
         mma_ts_tf32(tmem + kTf32OCol, tmem + kTf32PHiCol + ks * 8, dDlo + bo, p.idesc2, 1u);
@@ -269,7 +284,7 @@ __global__ void __launch_bounds__(kTf32Threads, 1)
     phase ^= 1u;
     ptx::tc_fence_after();
 #pragma unroll
-    for (int c0 = 0; c0 < 64; c0 += 16) {
+    for (int c0 = 0; c0 < kOC; c0 += 16) {
       if (c0 < p.TLP) {
         uint32_t r[16];
         ptx::tmem_ld16(tO + c0, r);
@@ -284,7 +299,7 @@ __global__ void __launch_bounds__(kTf32Threads, 1)
     float* e = E + beta * p.bs_e + static_cast<int64_t>(m0 + row) * p.ld_e;
     const float inv = p.op == 2 ? (l_run > 0.f ? 1.0f / l_run : 0.f) : 1.0f;
 #pragma unroll
-    for (int c = 0; c < 64; ++c)
+    for (int c = 0; c < kOC; ++c)
       if (c < p.L) e[c] = o[c] * inv;
   }
   ptx::tc_fence_before();

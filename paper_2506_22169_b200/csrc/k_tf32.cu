@@ -4,11 +4,16 @@
 
 namespace mbci {
 
-const void* tf32_fn() { return (const void*)k_chain_tf32; }
+const void* tf32_fn(bool wide) {
+  return wide ? (const void*)k_chain_tf32<TfWide> : (const void*)k_chain_tf32<TfSmall>;
+}
 
-cudaError_t launch_tf32(unsigned grid, cudaStream_t st, const float* A, const float* B, const float* D, float* E,
-                        const Tf32Params& p) {
-  k_chain_tf32<<<grid, kTf32Threads, kTf32Smem, st>>>(A, B, D, E, p);
+cudaError_t launch_tf32(bool wide, unsigned grid, cudaStream_t st, const float* A, const float* B, const float* D,
+                        float* E, const Tf32Params& p) {
+  if (wide)
+    k_chain_tf32<TfWide><<<grid, kTf32Threads, kTf32WideSmem, st>>>(A, B, D, E, p);
+  else
+    k_chain_tf32<TfSmall><<<grid, kTf32Threads, kTf32Smem, st>>>(A, B, D, E, p);
   return cudaGetLastError();
 }
 

@@ -36,10 +36,10 @@ Tc5Kernel pick_tc6_bf16(int kch, int bl, int emu);
 inline Tc5Kernel pick_tc6(bool bf16, int kch, int bl, int emu) {
   return bf16 ? pick_tc6_bf16(kch, bl, emu) : pick_tc6_f16(kch, bl, emu);
 }
-// kernel 7 (k_tf32.cu): fp32 on tcgen05, 3xTF32
-const void* tf32_fn();
-cudaError_t launch_tf32(unsigned grid, cudaStream_t st, const float* A, const float* B, const float* D, float* E,
-                        const Tf32Params& p);
+// kernel 7 (k_tf32.cu): fp32 on tcgen05, 3xTF32; wide = the K, L <= 128 variant (32-key tiles)
+const void* tf32_fn(bool wide);
+cudaError_t launch_tf32(bool wide, unsigned grid, cudaStream_t st, const float* A, const float* B, const float* D,
+                        float* E, const Tf32Params& p);
 // kernel 1, CUDA cores (k_simt.cu): dtype 0 f32, 1 f16, 2 bf16
 const void* simt_fn(int dtype);
 cudaError_t launch_simt(int dtype, unsigned grid, int smem, cudaStream_t st, const void* A, const void* B,

@@ -276,29 +276,31 @@ int enumerate_plans(const mbci_chain_desc_t& d, const mbci_hw_t& hw,
     }
   } else {
     // fp32 on tcgen05 (kernel 7, 3xTF32, chain_tf32.cuh): one CTA per (β, 128-row tile), 64-key
-    // tiles, K, L <= 64, any strides.  Scored from its synchronous per-tile structure (load +
+    // tiles for K, L <= 64 and 32-key tiles up to K, L <= 128, any strides.  Scored from its synchronous per-tile structure (load +
     // split, GEMM1, op, GEMM2 ~1.2 us per tile on a CTA) and ranked ahead of the CUDA-core path.
-    const bool tf32_ok = d.dtype == MBCI_F32 && d.K >= 1 && d.K <= 64 && d.L <= 64 && d.N >= 1 &&
+    const bool tf32_ok = d.dtype == MBCI_F32 && d.K >= 1 && d.K <= 128 && d.L <= 128 && d.N >= 1 &&
                          d.batch * cdiv(d.M, 128) <= (int64_t(1) << 31) - 1;
+    const bool tf32_wide = d.K > 64 || d.L > 64;   // 32-key tiles, 128 O columns
     if (tf32_ok) {
       mbci_plan_t p{};
       p.kernel = 7;
       p.BM = 128;
-      p.BN = 64;
+      p.BN = tf32_wide ? 32 : 64;
       p.TK = static_cast<int32_t>(cdiv(d.K, 8) * 8);
       p.TL = static_cast<int32_t>(std::max<int64_t>(16, cdiv(d.L, 16) * 16));
       p.stages = 1;
-      p.smem_bytes = 2 * (2 * 128 * 128 + 2 * 64 * 128 + 2 * 64 * 128) + 1024;
+      p.smem_bytes = tf32_wide ? 2 * (4 * 128 * 128 + 4 * 32 * 128 + 1 * 128 * 128) + 1024
+                               : 2 * (2 * 128 * 128 + 2 * 64 * 128 + 2 * 64 * 128) + 1024;
       p.tmem_cols = 256;
       double t[5];
-      model_terms(d.batch, d.M, d.N, d.K, d.L, 128, 64, p.TK, p.TL, s, hw, t);
+      model_terms(d.batch, d.M, d.N, d.K, d.L, 128, p.BN, p.TK, p.TL, s, hw, t);
       p.t_mem = t[0];
       p.t_comp = t[1];
       p.alpha = t[2];
       p.t_estm = t[3];
       p.n_block = d.batch * cdiv(d.M, 128);
       const double waves = std::ceil(static_cast<double>(p.n_block) / hw.n_sm);
-      p.t_b200 = waves * static_cast<double>(cdiv(d.N, 64)) * 1.2e-6 * (1.965e9 / hw.clock_hz) + 3.0e-6;
+      p.t_b200 = waves * static_cast<double>(cdiv(d.N, p.BN)) * 1.2e-6 * (1.965e9 / hw.clock_hz) + 3.0e-6;
       out.push_back(p);
     }
     const int64_t smem = d.N * 4 + 64;

@@ -149,7 +149,7 @@ def test_bert_base_prefers_full_L_tile(m):
 
 
 def test_fp32_goes_to_tf32x3_tensor_cores_and_misaligned_to_cuda_cores(m):
-    """fp32 (north_star (3)): kernel 7 (tcgen05 kind::tf32, 3xTF32) first whenever 1 <= K, L <= 64,
+    """fp32 (north_star (3)): kernel 7 (tcgen05 kind::tf32, 3xTF32) first whenever 1 <= K, L <= 128,
     the CUDA-core kernel 1 behind it as the fallback; 16-bit rows that break TMA's 16-B rule and fp32
     shapes outside kernel 7 go to kernel 1 only."""
     st, plans = m.plan_enumerate(m.make_desc(1, 128, 128, 16, 16, "f32", "none"))
@@ -157,14 +157,17 @@ def test_fp32_goes_to_tf32x3_tensor_cores_and_misaligned_to_cuda_cores(m):
     assert plans[0].BM == 128 and plans[0].BN == 64 and plans[0].TK == 16 and plans[0].TL == 16
     st, plans = m.plan_enumerate(m.make_desc(3, 300, 200, 20, 40, "f32", "softmax", 0.2))
     assert st == m.MBCI_OK and [p.kernel for p in plans] == [7, 1] and plans[0].TK == 24 and plans[0].TL == 48
-    for K, L in ((80, 16), (16, 80), (0, 16)):
+    for K, L in ((80, 16), (16, 80), (128, 128)):   # the wide variant: 32-key tiles, 128 O columns
+        st, plans = m.plan_enumerate(m.make_desc(1, 128, 128, K, L, "f32", "none"))
+        assert st == m.MBCI_OK and [p.kernel for p in plans] == [7, 1] and plans[0].BN == 32
+    for K, L in ((136, 16), (16, 136), (0, 16)):
         st, plans = m.plan_enumerate(m.make_desc(1, 128, 128, K, L, "f32", "none"))
         assert st == m.MBCI_OK and [p.kernel for p in plans] == [1]
     st, plans = m.plan_enumerate(m.make_desc(2, 3, 5, 3, 3, "f16", "none"))   # K=3: 6-byte rows
     assert st == m.MBCI_OK and plans[0].kernel == 1
     st, plans = m.plan_enumerate(m.make_desc(1, 16, 10**6, 16, 16, "f32", "none"))  # C row > SMEM: kernel 7 only
     assert st == m.MBCI_OK and [p.kernel for p in plans] == [7]
-    st, plans = m.plan_enumerate(m.make_desc(1, 16, 10**6, 16, 80, "f32", "none"))
+    st, plans = m.plan_enumerate(m.make_desc(1, 16, 10**6, 16, 136, "f32", "none"))
     assert st == m.MBCI_ERR_UNSUPPORTED and plans == []
 
 
@@ -236,4 +239,4 @@ def test_large_K_L_plans_are_kernel0_with_live_k_loop_or_h_chunks(m, K, L):
             dch = (p.TL + 63) // 64
             assert p.smem_bytes >= p.stages * (16384 + p.BN * 128 + dch * p.BN * 128)
     fp32 = m.plan_enumerate(m.make_desc(1, 512, 512, K, L, "f32", "none", 1.0))[1]
-    assert [p.kernel for p in fp32] == ([7, 1] if K <= 64 and L <= 64 else [1])
+    assert [p.kernel for p in fp32] == ([7, 1] if K <= 128 and L <= 128 else [1])

@@ -3,8 +3,8 @@ compensation) with the fp64 oracle, through the C ABI.  Tolerance: BASELINE.json
 1e-5 (row-max-normalised, R10) on every case; integer chains must match RN(oracle) bit
 for bit (every TF32 split is exact: lo = 0, and every fp32 partial sum is an exact integer).
 
-Covers the C1 config, both B layouts, every op, ragged M / N / K / L (K not a multiple of 8, L not
-of 16, N not of 64), key padding (0, 1, partial and full lengths), the online-rescale path, negative
+Covers the C1 config, both B layouts, every op, ragged M / N / K / L up to 128 (the wide 32-key-tile
+variant for K or L > 64; K not a multiple of 8, L not of 16, N not of 64), key padding (0, 1, partial and full lengths), the online-rescale path, negative
 and zero scale, unaligned strides (kernel 7 reads global memory with scalar loads), agreement with
 the CUDA-core kernel, run-to-run determinism, and that the default fp32 plan is kernel 7.
 """
@@ -54,7 +54,7 @@ def test_default_fp32_plan_is_kernel7(mbci):
     assert oracle.row_max_error(e_f64(E, "f32"), oracle.chain(inp, "none", 1.0)) <= TOL
 
 
-@pytest.mark.parametrize("K", [8, 16, 40, 64])
+@pytest.mark.parametrize("K", [8, 16, 40, 64, 128])
 @pytest.mark.parametrize("b_layout", [0, 1])
 def test_integer_chain_bitwise(mbci, K, b_layout):
     inp = gen.make_chain_inputs(300 + K, "f32", 3, 200, 300, K, 48, b_layout, kind="int")
@@ -71,7 +71,8 @@ def test_ops_and_layouts(mbci, op, scale, b_layout):
 
 
 @pytest.mark.parametrize("M,N,K,L", [(1, 1, 1, 1), (129, 65, 9, 17), (300, 333, 20, 40), (100, 130, 24, 20),
-                                     (64, 1000, 64, 64), (257, 64, 63, 33)])
+                                     (64, 1000, 64, 64), (257, 64, 63, 33), (200, 300, 128, 128), (130, 77, 96, 40),
+                                     (64, 200, 24, 120)])
 def test_ragged_shapes(mbci, M, N, K, L):
     inp = gen.make_chain_inputs(M + N + K, "f32", 2, M, N, K, L, 1)
     check7(mbci, inp, "softmax", 1.0 / math.sqrt(K))
