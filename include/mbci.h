@@ -252,6 +252,22 @@ mbci_status_t mbci_model_terms(int64_t batch, int64_t M, int64_t N, int64_t K, i
                                int64_t TM, int64_t TN, int64_t TK, int64_t TH, int32_t elem_bytes,
                                const mbci_hw_t* hw, double out[5]);
 
+/* The paper's search space for the two-GEMM chain and its pruning funnel (Fig. 7):
+ * 26 tiling expressions x tile vectors of multiples of 16, then Rule 1
+ * (deduplicate by the sub-tiling expression left after deleting the blockIdx-bound loops m and h,
+ * P:285), Rule 2 (drop `kn`-type classes), Rule 3 (padding) and Rule 4 (Eq. 1 over
+ * the A, B, C, D, E tiles x elem_bytes > 1.2 shm_max); R21.  Counts
+ * are candidates (expression class x tile vector) retained after each rule.  Host only.
+ * INVALID on non-positive sizes or a NULL out; UNSUPPORTED if more than 2^30 tile vectors survive
+ * Rule 3 (the Rule-4 pass enumerates them). */
+typedef struct {
+  int32_t expr_raw, expr_rule1, expr_rule2;                 /* tiling expressions / classes */
+  int64_t tile_vectors, tile_vectors_rule3, tile_vectors_rule4;
+  int64_t raw, after_rule1, after_rule2, after_rule3, after_rule4;
+} mbci_funnel_t;
+mbci_status_t mbci_prune_funnel(int64_t M, int64_t N, int64_t K, int64_t H, int32_t elem_bytes,
+                                int64_t shm_max, mbci_funnel_t* out);
+
 #ifdef __cplusplus
 }
 #endif

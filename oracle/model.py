@@ -143,3 +143,52 @@ def chain_estimate(batch, M, N, K, L, TM, TN, TK, TH, s, W, P, n_sm):
     mem, comp, nb = chain_schedule(batch, M, N, K, L, TM, TN, TK, TH, s)
     tm, tc, a = t_mem(mem, W), t_comp(comp, P), alpha(nb, n_sm)
     return {"t_mem": tm, "t_comp": tc, "alpha": a, "t_estm": t_estm(tm, tc, a), "n_block": nb}
+
+
+# ---- §III-C pruning (Rules 1-4) and the Fig. 7 funnel ----------------------
+# PAPER.md:283-312.  Readings (R21): Rule 1 binds the spatial loops of the final output
+# (m and h of E) to blockIdx and deletes them wherever they appear (the paper's own example
+# "both mhnk and mnkh yield the same sub-tiling expression nk"); Rule 2 rejects a class
+# whose producer reduction k encloses the producer's spatial loop n ("reduced loop positioned
+# outside the spatial loops", Fig. 6(b): `kn`); Rule 3 as rule3_reject on every axis;
+# Rule 4 with Eq. (1) over the five in-block tiles A (TM x TK), B (TK x TN), C (TM x TN),
+# D (TN x TH), E (TM x TH) times the element size, rejected when > 1.2 Shm_max.
+def sub_tiling_expression(expr: str, bound: str = "mh") -> str:
+    """Rule 1 key: delete the blockIdx-bound loops; an emptied or one-child Seq collapses."""
+    out = "".join(c for c in expr if c not in bound)
+    out = out.replace("(,", "(").replace(",)", ")").replace("()", "")
+    if "(" in out and "," not in out:   # n(k) stays a Seq of one child: print as n(k)
+        pass
+    return out
+
+
+def rule2_reject(key: str) -> bool:
+    """the producer C's reduction loop k outside its spatial loop n caches many C tiles."""
+    return "k" in key and "n" in key and key.index("k") < key.index("n")
+
+
+def prune_funnel(M: int, N: int, K: int, H: int, elem_bytes: int, shm_max: float):
+    """Fig. 7: candidate counts (expression x tile vector) after each rule."""
+    import numpy as np
+    exprs = deep_expressions() + flat_expressions()
+    keys = []
+    for e in exprs:   # first writer wins (canonical order: deep permutations, then flat)
+        k = sub_tiling_expression(e)
+        if k not in keys:
+            keys.append(k)
+    kept = [k for k in keys if not rule2_reject(k)]
+    opts = [tile_options(d) for d in (M, N, K, H)]
+    v_raw = math.prod(len(o) for o in opts)
+    surv = [np.array([t for t in o if not rule3_reject(d, t)], dtype=np.float64)
+            for o, d in zip(opts, (M, N, K, H))]
+    v3 = math.prod(len(s) for s in surv)
+    TM, TN, TK, TH = np.meshgrid(*surv, indexing="ij")
+    shm = (TM * TK + TK * TN + TM * TN + TN * TH + TM * TH) * elem_bytes   # Eq. (1)
+    v4 = int(np.count_nonzero(~(shm > 1.2 * shm_max)))
+    return {
+        "expr_raw": len(exprs), "expr_rule1": len(keys), "expr_rule2": len(kept), "keys": keys,
+        "tile_vectors": v_raw, "tile_vectors_rule3": v3, "tile_vectors_rule4": v4,
+        "raw": len(exprs) * v_raw, "after_rule1": len(keys) * v_raw,
+        "after_rule2": len(kept) * v_raw, "after_rule3": len(kept) * v3,
+        "after_rule4": len(kept) * v4,
+    }

@@ -12,7 +12,7 @@ LIB = os.path.join(HERE, "libmbci.so")
 LIB_TRACE = os.path.join(HERE, "libmbci_trace.so")
 # api.cu (ABI + host logic), selector.cpp, and one translation unit per kernel family / dtype
 # (k_*.cu), compiled in parallel and linked into one shared library.
-SOURCES = [os.path.join(CSRC, "api.cu"), os.path.join(CSRC, "selector.cpp"), os.path.join(CSRC, "search.cpp")] + sorted(
+SOURCES = [os.path.join(CSRC, f) for f in ("api.cu", "selector.cpp", "search.cpp", "prune.cpp")] + sorted(
     os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.startswith("k_") and f.endswith(".cu"))
 DEPS = SOURCES + [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith((".cuh", ".h"))] + [
     os.path.join(os.path.dirname(HERE), "include", "mbci.h")]

@@ -1162,4 +1162,13 @@ mbci_status_t mbci_model_terms(int64_t batch, int64_t M, int64_t N, int64_t K, i
   return MBCI_OK;
 }
 
+mbci_status_t mbci_prune_funnel(int64_t M, int64_t N, int64_t K, int64_t H, int32_t elem_bytes, int64_t shm_max,
+                                mbci_funnel_t* out) {
+  if (!out || M <= 0 || N <= 0 || K <= 0 || H <= 0 || elem_bytes <= 0 || shm_max <= 0)
+    return fail(MBCI_ERR_INVALID, "bad funnel arguments");
+  const mbci_status_t st = prune_funnel(M, N, K, H, elem_bytes, shm_max, out);
+  if (st != MBCI_OK) return fail(st, "more than 2^30 tile vectors survive Rule 3");
+  return MBCI_OK;
+}
+
 }  // extern "C"

@@ -36,5 +36,8 @@ bool tc5_layout(int32_t k_steps, int32_t TL, int32_t stages, int32_t b_layout, T
 int enumerate_plans(const mbci_chain_desc_t& d, const mbci_hw_t& hw,
                     std::vector<mbci_plan_t>& out, bool rule3 = true);
 void hw_default(mbci_hw_t* hw);
+// PAPER.md Fig. 7 funnel over the paper's own search space (prune.cpp).
+mbci_status_t prune_funnel(int64_t M, int64_t N, int64_t K, int64_t H, int32_t elem_bytes, int64_t shm_max,
+                           mbci_funnel_t* f);
 
 }  // namespace mbci

@@ -108,6 +108,14 @@ class mbci_chain3_desc_t(ctypes.Structure):
 _lib.mbci_chain3_create.argtypes = [_P(mbci_chain3_desc_t), ctypes.c_int, _P(_vp)]
 _lib.mbci_chain3_run.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
 
+class mbci_funnel_t(ctypes.Structure):
+    _fields_ = [("expr_raw", ctypes.c_int32), ("expr_rule1", ctypes.c_int32), ("expr_rule2", ctypes.c_int32)] + [
+        (n, ctypes.c_int64) for n in ("tile_vectors", "tile_vectors_rule3", "tile_vectors_rule4", "raw",
+                                      "after_rule1", "after_rule2", "after_rule3", "after_rule4")]
+
+
+_lib.mbci_prune_funnel.argtypes = [ctypes.c_int64] * 4 + [ctypes.c_int32, ctypes.c_int64, _P(mbci_funnel_t)]
+
 mbci_measure_fn = ctypes.CFUNCTYPE(ctypes.c_double, _P(mbci_plan_t), _vp)
 _lib.mbci_plan_search.argtypes = [_P(mbci_chain_desc_t), _P(mbci_hw_t), _P(mbci_search_params_t), mbci_measure_fn,
                                   _vp, _P(mbci_plan_t), _P(mbci_search_result_t), _P(ctypes.c_double)]
@@ -116,7 +124,7 @@ for _f in ("mbci_chain_create", "mbci_chain_create_with_plan", "mbci_chain_run",
            "mbci_chain_set_trace",
            "mbci_chain_destroy", "mbci_chain_plan", "mbci_chain_describe", "mbci_plan_enumerate",
            "mbci_plan_select", "mbci_model_terms", "mbci_plan_search", "mbci_chain_search_stats",
-           "mbci_chain3_create", "mbci_chain3_run"):
+           "mbci_chain3_create", "mbci_chain3_run", "mbci_prune_funnel"):
     getattr(_lib, _f).restype = _st
 
 EXPORTED = ["mbci_chain_create", "mbci_chain_create_with_plan", "mbci_chain_run", "mbci_chain_run_host",
@@ -124,7 +132,7 @@ EXPORTED = ["mbci_chain_create", "mbci_chain_create_with_plan", "mbci_chain_run"
             "mbci_chain_set_trace",
             "mbci_status_string", "mbci_last_error", "mbci_abi_version", "mbci_hw_default",
             "mbci_plan_enumerate", "mbci_plan_select", "mbci_model_terms", "mbci_plan_search",
-            "mbci_chain_search_stats", "mbci_chain3_create", "mbci_chain3_run"]
+            "mbci_chain_search_stats", "mbci_chain3_create", "mbci_chain3_run", "mbci_prune_funnel"]
 
 # ---- same names as the C ABI ---------------------------------------------------------------
 mbci_chain_create = _lib.mbci_chain_create
@@ -147,6 +155,7 @@ mbci_plan_search = _lib.mbci_plan_search
 mbci_chain_search_stats = _lib.mbci_chain_search_stats
 mbci_chain3_create = _lib.mbci_chain3_create
 mbci_chain3_run = _lib.mbci_chain3_run
+mbci_prune_funnel = _lib.mbci_prune_funnel
 
 
 def plan_search(desc, measure, hw=None, N=512, n=8, eps=0.01, seed=1, max_rounds=64, model=0):
@@ -212,6 +221,12 @@ def model_terms(batch, M, N, K, L, TM, TN, TK, TH, s, hw=None):
     check(mbci_model_terms(batch, M, N, K, L, TM, TN, TK, TH, s,
                            ctypes.byref(hw) if hw is not None else None, out), "mbci_model_terms")
     return {"t_mem": out[0], "t_comp": out[1], "alpha": out[2], "t_estm": out[3], "n_block": out[4]}
+
+
+def prune_funnel(M, N, K, H, elem_bytes=2, shm_max=232448) -> dict:
+    f = mbci_funnel_t()
+    check(mbci_prune_funnel(M, N, K, H, elem_bytes, shm_max, ctypes.byref(f)), "mbci_prune_funnel")
+    return {name: getattr(f, name) for name, _ in f._fields_}
 
 
 _TORCH_DT = None

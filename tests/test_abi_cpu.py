@@ -240,3 +240,21 @@ def test_large_K_L_plans_are_kernel0_with_live_k_loop_or_h_chunks(m, K, L):
             assert p.smem_bytes >= p.stages * (16384 + p.BN * 128 + dch * p.BN * 128)
     fp32 = m.plan_enumerate(m.make_desc(1, 512, 512, K, L, "f32", "none", 1.0))[1]
     assert [p.kernel for p in fp32] == ([7, 1] if K <= 128 and L <= 128 else [1])
+
+
+@pytest.mark.parametrize("shape", [(1024, 1024, 512, 512), (64, 64, 32, 32), (1000, 1000, 500, 500),
+                                   (512, 512, 64, 64), (4096, 4096, 128, 128), (197, 197, 64, 64)])
+@pytest.mark.parametrize("shm", [101376, 166912, 232448])
+def test_prune_funnel_matches_oracle(m, shape, shm):
+    """mbci_prune_funnel (csrc/prune.cpp) against oracle.model.prune_funnel (Fig. 7)."""
+    from oracle import model
+    got = m.prune_funnel(*shape, 2, shm)
+    ref = model.prune_funnel(*shape, 2, shm)
+    for k, v in got.items():
+        assert v == ref[k], (k, v, ref[k])
+
+
+def test_prune_funnel_errors(m):
+    f = m.mbci_funnel_t()
+    assert m.mbci_prune_funnel(0, 1, 1, 1, 2, 1000, ctypes.byref(f)) == 1
+    assert m.mbci_prune_funnel(16, 16, 16, 16, 2, 1000, None) == 1

@@ -406,3 +406,59 @@ def test_chain3_brute_force_numpy():
                 e = (p / p.sum()) @ D[b, :lim]
                 g = 0.5 * 1.7 * e * (1.0 + sp_erf(1.7 * e / math.sqrt(2.0)))
                 assert np.max(np.abs(got[b, m] - g @ Ff[b])) < 1e-12
+
+
+# ---- Fig. 7 pruning funnel (§III-C) -------------------------------------------------
+def _funnel_golden():
+    g = {}
+    for line in _read_golden("funnel.txt"):
+        lhs, rhs = line.split("=")
+        g[lhs.strip()] = rhs.strip()
+    return g
+
+
+def test_funnel_rule1_rule2_against_paper_examples():
+    g = _funnel_golden()
+    a, b, key = g["rule1_same_class"].split()
+    assert model.sub_tiling_expression(a) == key == model.sub_tiling_expression(b)
+    assert model.sub_tiling_expression("mhkn") == g["rule2_rejected_class"]   # Fig. 6 caption: "kn"
+    assert model.rule2_reject(g["rule2_rejected_class"])
+    assert not model.rule2_reject(key)
+    # every deep permutation keeps n and k in its own order; both flat ones keep n outside k
+    for e in model.deep_expressions():
+        k = model.sub_tiling_expression(e)
+        assert k == ("nk" if e.index("n") < e.index("k") else "kn")
+    assert {model.sub_tiling_expression(e) for e in model.flat_expressions()} == {"n(k)"}
+
+
+def test_funnel_counts_against_paper():
+    g = _funnel_golden()
+    f = model.prune_funnel(1024, 1024, 512, 512, 2, 166912)   # A100 (the paper's platform): 163 KB
+    assert f["raw"] == int(g["raw_candidates"])
+    assert f["expr_raw"] == int(g["expressions"])
+    assert f["expr_rule1"] == 3 and f["expr_rule2"] == 2 and f["keys"] == ["nk", "kn", "n(k)"]
+    # Rule 3 on power-of-2 dims keeps exactly the power-of-2 tiles 16 .. dim (closed form)
+    closed = 1
+    for d in (1024, 1024, 512, 512):
+        closed *= int(math.log2(d // 16)) + 1
+    assert f["tile_vectors_rule3"] == closed == 7 * 7 * 6 * 6
+    assert 1 - f["tile_vectors_rule3"] / f["tile_vectors"] >= float(g["rule3_min_discard"])
+    assert int(g["final_order_low"]) <= f["after_rule4"] <= int(g["final_order_high"])
+    # Rule 4 brute force: Eq. (1) over the 1764 survivors by plain loops
+    surv = [[t for t in model.tile_options(d) if not model.rule3_reject(d, t)] for d in (1024, 1024, 512, 512)]
+    kept = sum(1 for tm in surv[0] for tn in surv[1] for tk in surv[2] for th in surv[3]
+               if not model.rule4_reject(model.shm_estm([(tm, tk), (tk, tn), (tm, tn), (tn, th), (tm, th)]) * 2, 166912))
+    assert f["tile_vectors_rule4"] == kept
+
+
+def test_funnel_limits_and_ragged_dims():
+    # Rule 4 with an unbounded budget rejects nothing, with a 1-byte budget everything
+    f = model.prune_funnel(256, 256, 64, 64, 2, 10**12)
+    assert f["tile_vectors_rule4"] == f["tile_vectors_rule3"]
+    assert model.prune_funnel(256, 256, 64, 64, 2, 1)["tile_vectors_rule4"] == 0
+    # SPEC.md:158 tiny space: 26 x 4*4*2*2
+    assert model.prune_funnel(64, 64, 32, 32, 2, 232448)["raw"] == 1664
+    # ragged dim 1000 (not a power of 2): a tile survives iff its padding is < 50 elements
+    keep = [t for t in model.tile_options(1000) if not model.rule3_reject(1000, t)]
+    assert keep == [t for t in range(16, 1009, 16) if math.ceil(1000 / t) * t - 1000 < 50]
+    assert 1008 in model.tile_options(1000) and 1008 in keep   # 8 / 1000 padding
