@@ -426,6 +426,152 @@ def run_cuda(args, rank, world, local_rank):
     ch.close()
 
 
+def run_split(args, rank, world, local_rank):
+    """--split-n P: the key axis cut into P ranges.  world > 1: ranks form
+    world / P groups of P consecutive ranks; a group shares a β range (strong / weak as usual), each
+    rank runs mbci_chain_run_partial on its key range (B, D strided views at the range's first key),
+    the group all-gathers the partial E and row log-sum-exp over NCCL and mbci_merge_partials reduces
+    them — the path's one exchange step, inside the timed region (eager launches: the NCCL calls are
+    not graph-captured).  world == 1: the P partial launches run back to back on one GPU, then the
+    merge (graph-captured) — the cost of split-N against the single fused launch."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import mbci_inputs as gen
+    from paper_2506_22169_b200 import mbci, sharding
+
+    P = args.split_n
+    if world > 1 and world % P:
+        raise SystemExit("--split-n must divide the number of ranks")
+    name = args.config
+    dtype, b, M, N, K, L, op, desc, s, bytes_, flops, exps = cfg_numbers(name)
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    tdt = {"f32": torch.float32, "f16": torch.float16, "bf16": torch.bfloat16}[dtype]
+    b_layout = 1 if op == "softmax" else 0
+    sc = 1.0 / math.sqrt(K) if op == "softmax" else 1.0
+    sig = (1.0, 1.0, 1.0) if op == "softmax" else (1.0, 1.0 / math.sqrt(K), 1.0 / math.sqrt(N))
+    groups = world // P if world > 1 else 1
+    grp, part = sharding.split_grid(rank, world, P) if world > 1 else (0, None)
+    global_b = b if args.scaling == "strong" else b * groups
+    lo, hi = sharding.shard_range(global_b, grp, groups)
+    nb = hi - lo
+    inp = gen.make_chain_inputs(args.seed, dtype, nb, M, N, K, L, b_layout, sigmas=sig, batch_start=lo)
+    mine = [part] if world > 1 else list(range(P))
+    spans = [sharding.key_range(N, p, P) for p in range(P)]
+
+    def to_t(bits):
+        return torch.from_numpy(bits.view(np.int32 if dtype == "f32" else np.int16)).view(tdt)
+    hA, hB, hD = to_t(inp.A), to_t(inp.B), to_t(inp.D)
+    step_bytes = nb * (M * K + K * N + N * L + M * L) * s // (P if world > 1 else 1)
+    rot = max(2, math.ceil(2 * L2_BYTES / max(1, nb * (M * K + K * N + N * L + M * L) * s)) + 1)
+    sets = [(hA.to(dev), hB.to(dev), hD.to(dev)) for _ in range(rot)]
+    strides = ({"ld_b": K, "bs_b": N * K} if b_layout == 1 else {"ld_b": N, "bs_b": K * N})
+    strides.update(ld_d=L, bs_d=N * L)
+    chs = [mbci.Chain(nb, M, spans[p][1] - spans[p][0], K, L, dtype, op, sc, b_layout=b_layout, device=local_rank,
+                      strides=strides) for p in mine]
+    E_parts = torch.empty(len(mine), nb, M, L, dtype=tdt, device=dev)
+    lse = torch.empty(len(mine), nb, M, dtype=torch.float32, device=dev)
+    E = torch.empty(nb, M, L, dtype=tdt, device=dev)
+    sub = None
+    if world > 1:
+        for ranks in sharding.key_groups(world, P):   # every rank creates every group, same order
+            gh = dist.new_group(ranks)
+            if rank in ranks:
+                sub = gh
+    stream = torch.cuda.Stream(dev)
+
+    def step(i):
+        A, B, D = sets[i % rot]
+        for j, p in enumerate(mine):
+            n0, n1 = spans[p]
+            Bv = B[:, n0:n1, :] if b_layout == 1 else B[:, :, n0:n1]
+            chs[j].run_partial(A, Bv, D[:, n0:n1, :], E_parts[j], lse[j] if op == "softmax" else None, None, n0,
+                               stream=stream)
+        if world > 1:
+            Ea, la = sharding.gather_partials(E_parts[0], lse[0] if op == "softmax" else None, group=sub)
+        else:
+            Ea, la = E_parts, (lse if op == "softmax" else None)
+        mbci.merge_partials(Ea, la, E, op, stream=stream)
+
+    with torch.cuda.stream(stream):
+        for i in range(args.warmup):
+            step(i)
+    stream.synchronize()
+    graph = None
+    if world == 1:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            for i in range(args.steps):
+                step(i)
+    sampler = ClockSampler(_gpu_id(local_rank))
+    sampler.start()
+    time.sleep(0.3)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_load0 = time.time()
+    ev0.record(stream)
+    with torch.cuda.stream(stream):
+        if graph is not None:
+            graph.replay()
+        else:
+            for i in range(args.steps):
+                step(i)
+    ev1.record(stream)
+    ev1.synchronize()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t_load1 = time.time()
+    time.sleep(0.25)
+    sampler.stop()
+    ms_per_step = sharding.max_over_ranks(ev0.elapsed_time(ev1)) / args.steps
+    total_bytes = sharding.sum_over_ranks(step_bytes)
+    gbs = total_bytes / (ms_per_step * 1e-3) / 1e9
+    # after timing: the merged rows of every β group against the oracle (rank 0)
+    with torch.cuda.stream(stream):
+        step(0)
+    stream.synchronize()
+    E_bits = E.view(torch.int32 if dtype == "f32" else torch.int16)
+    if world > 1:
+        counts = [sharding.shard_range(global_b, r // P, groups)[1] - sharding.shard_range(global_b, r // P, groups)[0]
+                  for r in range(world)]
+        allE = sharding.gather_shards(E_bits, counts)
+        offs = np.cumsum([0] + counts)
+        E_all = torch.cat([allE[offs[g * P]: offs[g * P] + counts[g * P]] for g in range(groups)]) if rank == 0 else None
+    else:
+        E_all = E_bits
+    if rank != 0:
+        return
+    E_all = E_all.cpu().numpy().view(np.uint32 if dtype == "f32" else np.uint16)
+    sl = sorted({0, global_b - 1} | {sharding.shard_range(global_b, g, groups)[0] for g in range(groups)})[:16]
+    gcheck = gather_check(name, args.seed, E_all, sl) if not args.no_cpu_baseline else None
+    clocks = sampler.summary(t_load0, t_load1)
+    pk = peaks()
+    line = {
+        "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_per_step, "us_per_chain": ms_per_step * 1e3, "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None, "dtype": dtype, "data": "synthetic",
+        "mbci_env": {k: v for k, v in sorted(os.environ.items()) if k.startswith("MBCI_")},
+        "config": {"workload": desc, "name": name, "split_n": P, "beta_groups": groups, "global_batch_heads": global_b,
+                   "batch_heads_per_group": nb, "key_ranges": spans, "M": M, "N": N, "K": K, "L": L, "op": op,
+                   "parallelism": f"dp{groups} x split-N {P} (all-gather of partial E + lse, merge kernel)",
+                   "timing": ("K steps in one CUDA graph" if world == 1 else "K eager steps (NCCL inside)")
+                             + ", CUDA events on the launch stream, max over ranks",
+                   "plans": [c.describe() for c in chs]},
+        "roofline": {"bound": "hbm", "achieved": gbs / world, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                     "frac": gbs / world / pk["hbm_gbs"], "traffic": None, "peak_src": pk["src"]},
+        "cpu_baseline": None, "e2e": None,
+        "gpu_launches": (len(mine) + 1) * args.steps, "clocks": clocks, "gather_check": gcheck,
+    }
+    print(json.dumps(line), flush=True)
+    for c in chs:
+        c.close()
+
+
 def _gpu_id(local_rank):
     try:
         import torch
@@ -485,6 +631,8 @@ def main():
     ap.add_argument("--sustain", type=float, default=1.0, help="seconds of untimed load for the clock sampler")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--split-n", type=int, default=1,
+                    help="cut the key axis into P ranges (SURVEY f1): groups of P ranks all-gather and merge")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -513,6 +661,8 @@ def main():
               f"NCCL communicator ready, nranks={int(t.item())}, nccl {'.'.join(map(str, torch.cuda.nccl.version()))}",
               file=sys.stderr, flush=True)
     try:
+        if args.split_n > 1:
+            return run_split(args, rank, world, local_rank)
         run_cuda(args, rank, world, local_rank)
     finally:
         if world > 1:

@@ -153,6 +153,29 @@ mbci_status_t mbci_chain_run(mbci_chain_t h, const void* A, const void* B, const
 mbci_status_t mbci_chain_run_host(mbci_chain_t h, const void* A, const void* B, const void* D,
                                   void* E, const int32_t* valid_len, void* stream);
 
+/* ---- split-N: the key axis n cut into disjoint ranges ---------------------
+ * One part of the chain over the keys [key_offset, key_offset + N) of a longer sequence: the
+ * handle's desc has N = this part's key count, and B / D point at its first key row.  E receives
+ * the part's own result (softmax normalised over ITS keys); for SOFTMAX, lse
+ * (DEVICE, fp32 [batch][M] packed, owned by the caller) receives the natural-log row
+ * log-sum-exp ln Σ_{n in part} exp(scale · C[m,n]) over the part's unmasked keys (−inf when none).
+ * valid_len (KEY_PADDING) counts keys of the FULL sequence; the part sees
+ * clamp(valid_len[β] − key_offset, 0, N).  Other ops ignore lse (it may be NULL).  Errors as
+ * mbci_chain_run, plus INVALID (SOFTMAX without lse, key_offset < 0 or > 2^31 − 1) and
+ * UNSUPPORTED (the causal mask, three-contraction handles, kernel-6 plans). */
+mbci_status_t mbci_chain_run_partial(mbci_chain_t h, const void* A, const void* B, const void* D, void* E,
+                                     float* lse, const int32_t* valid_len, int64_t key_offset, void* stream);
+
+/* The reduce step of split-N: E[β,m,:] from `parts` partial results over disjoint key ranges,
+ * E_parts [parts][batch][M][L] and lse_parts [parts][batch][M] packed (DEVICE; e.g. gathered
+ * from the ranks over NCCL), E [batch][M][L] packed (DEVICE, must not alias the parts).
+ * SOFTMAX: E = Σ_r w_r E_r / Σ_r w_r with w_r = exp(lse_r − max lse), exact in real arithmetic
+ * (each E_r·exp(lse_r) is the part's unnormalised product; a row with no valid key anywhere gives
+ * 0).  NONE / SCALE / RELU / GELU: E = Σ_r E_r.  fp32 arithmetic, one rounding to dtype
+ * (mbci_dtype_t).  Asynchronous on stream.  INVALID on bad sizes / enums / NULL buffers. */
+mbci_status_t mbci_merge_partials(int32_t parts, const void* E_parts, const float* lse_parts, void* E,
+                                  int64_t batch, int64_t M, int64_t L, int32_t dtype, int32_t op, void* stream);
+
 /* Free the handle and its device scratch.  The caller must have synchronised every stream
  * the handle ran on.  NULL is a no-op. */
 mbci_status_t mbci_chain_destroy(mbci_chain_t h);

@@ -62,6 +62,8 @@ def lib():
                                     ctypes.c_double, ctypes.c_int, vp, ctypes.c_int, ctypes.c_int,
                                     ctypes.c_double, ctypes.c_int]
         L.oracle_chain3.restype = ctypes.c_int
+        L.oracle_row_lse.argtypes = [vp, vp, dp, ctypes.c_int, i64, i64, i64, i64, ctypes.c_double, ctypes.c_int,
+                                     vp, ctypes.c_int]
         L.oracle_decode_array.argtypes = [vp, ctypes.c_int, i64, dp]
         L.oracle_decode_array.restype = ctypes.c_int
         L.oracle_max_threads.restype = ctypes.c_int
@@ -120,6 +122,20 @@ def chain(inp, op: str, scale: float = 1.0, valid_len=None, rows=None,
     if rc != 0:
         raise ValueError("oracle_chain rejected its arguments")
     return (E, Cp) if want_cprime else E
+
+
+def row_lse(inp, scale: float, valid_len=None, nthreads: int = 0) -> np.ndarray:
+    """fp64 [batch, M]: ln sum_{n < valid} exp(scale * (A.B)[m, n]) (-inf without a valid key) — the
+    statistic of a split-N partial."""
+    A = np.ascontiguousarray(inp.A)
+    B = np.ascontiguousarray(inp.B)
+    vl = None if valid_len is None else np.ascontiguousarray(valid_len, dtype=np.int32)
+    out = np.empty((inp.batch, inp.M), dtype=np.float64)
+    rc = lib().oracle_row_lse(_ptr(A), _ptr(B), _ptr(out), DTYPE_CODE[inp.dtype], inp.batch, inp.M, inp.N, inp.K,
+                              float(scale), inp.b_layout, _ptr(vl), int(nthreads))
+    if rc != 0:
+        raise ValueError("oracle_row_lse rejected its arguments")
+    return out
 
 
 def chain3(inp, F, H: int, op: str, scale: float, op2: str, scale2: float = 1.0, valid_len=None,

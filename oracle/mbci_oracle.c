@@ -232,6 +232,54 @@ int oracle_chain_ex(const void* A, const void* B, const void* D, double* E, int 
   return err ? -1 : 0;
 }
 
+/* Row log-sum-exp of the SOFTMAX op (the statistic a split-N partial result carries, SURVEY §8(f)
+ * f1): lse[β, m] = ln Σ_{n < v} exp(scale · C[m, n]) with C = A·B (step 2) and v the clamped
+ * valid_len (all N keys when NULL); −inf when v = 0.  Two-pass stable evaluation
+ * μ + ln Σ exp(z − μ), as chain_row's softmax.  lse is [batch, M].  Returns 0 or -1. */
+int oracle_row_lse(const void* A, const void* B, double* lse, int dtype, int64_t batch, int64_t M,
+                   int64_t N, int64_t K, double scale, int b_layout, const int32_t* valid_len,
+                   int nthreads) {
+  if (batch < 0 || M < 0 || N < 0 || K < 0 || dtype < 0 || dtype > 2 || b_layout < 0 || b_layout > 1) return -1;
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#else
+  (void)nthreads;
+#endif
+  int err = 0;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t beta = 0; beta < batch; ++beta) {
+    double* a = (double*)malloc((size_t)ORC_MAX1(M * K) * sizeof(double));
+    double* b = (double*)malloc((size_t)ORC_MAX1(K * N) * sizeof(double));
+    double* z = (double*)malloc((size_t)ORC_MAX1(N) * sizeof(double));
+    if (!a || !b || !z) {
+#pragma omp atomic write
+      err = 1;
+    } else {
+      decode_span(A, dtype, beta * M * K, M * K, a);
+      decode_span(B, dtype, beta * K * N, K * N, b);
+      const int64_t v = clamp_vlen(ORC_OP_SOFTMAX, valid_len, beta, N);
+      for (int64_t m = 0; m < M; ++m) {
+        double mu = -INFINITY;
+        for (int64_t n = 0; n < v; ++n) {
+          double acc = 0.0;
+          for (int64_t k = 0; k < K; ++k) acc += a[m * K + k] * (b_layout == 0 ? b[k * N + n] : b[n * K + k]);
+          z[n] = scale * acc;
+          if (z[n] > mu) mu = z[n];
+        }
+        if (mu == -INFINITY) {
+          lse[beta * M + m] = -INFINITY;
+        } else {
+          double Z = 0.0;
+          for (int64_t n = 0; n < v; ++n) Z += exp(z[n] - mu);
+          lse[beta * M + m] = mu + log(Z);
+        }
+      }
+    }
+    free(a); free(b); free(z);
+  }
+  return err ? -1 : 0;
+}
+
 /* Three-contraction chain: E3 [batch, M, H] = op2(op(A·B)·D) · F, F [batch, L, H] packed row-major
  * storage bits; op2 in {NONE, SCALE, RELU, GELU} with scale2; the rest as oracle_chain_ex.
  * Plain and unfused: the two-contraction row of steps 1-4, then steps 5-6 per row. */

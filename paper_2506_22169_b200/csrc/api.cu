@@ -370,7 +370,7 @@ mbci_status_t setup_plan(mbci_chain* h) {
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 mbci_status_t launch(mbci_chain* h, const void* A, const void* B, const void* D, void* E,
-                     const int32_t* valid_len, cudaStream_t st) {
+                     const int32_t* valid_len, cudaStream_t st, float* lse = nullptr, int32_t key_off = 0) {
   const mbci_chain_desc_t& d = h->d;
   if (d.batch == 0 || d.M == 0 || d.L == 0) return MBCI_OK;  // nothing to write
   if (!E) return fail(MBCI_ERR_INVALID, "E is NULL");
@@ -425,6 +425,8 @@ mbci_status_t launch(mbci_chain* h, const void* A, const void* B, const void* D,
     if (h->plan.kernel == 0) {
       TcParams t = h->tp;
       t.valid_len = vl;
+      t.key_off = key_off;
+      t.lse = lse;
       t.E = E;
       t.trace = h->trace;
       h->tc<<<(unsigned)h->plan.n_block, kThreads, h->plan.smem_bytes, st>>>(ent->ta, ent->tb, ent->td,
@@ -432,12 +434,16 @@ mbci_status_t launch(mbci_chain* h, const void* A, const void* B, const void* D,
     } else if (h->plan.kernel == 4) {
       Tc4Params t = h->tp4;
       t.valid_len = vl;
+      t.key_off = key_off;
+      t.lse = lse;
       t.E = E;
       t.trace = h->trace;
       h->tc4<<<(unsigned)h->grid2, kT4Threads, h->plan.smem_bytes, st>>>(ent->ta, ent->tb, ent->td, t);
     } else {
       Tc4Params t = h->tp4;
       t.valid_len = vl;
+      t.key_off = key_off;
+      t.lse = lse;
       t.E = E;
       t.trace = h->trace;
       cudaLaunchConfig_t cfg{};
@@ -456,6 +462,8 @@ mbci_status_t launch(mbci_chain* h, const void* A, const void* B, const void* D,
   } else if (h->plan.kernel == 7) {
     Tf32Params t = h->tp7;
     t.valid_len = vl;
+    t.key_off = key_off;
+    t.lse = lse;
     cudaError_t le = launch_tf32(h->plan.BN == 32, (unsigned)h->plan.n_block, st, (const float*)A, (const float*)B,
                                  (const float*)D, (float*)E, t);
     if (le != cudaSuccess) return cuda_fail(le, "kernel-7 launch");
@@ -470,6 +478,8 @@ mbci_status_t launch(mbci_chain* h, const void* A, const void* B, const void* D,
     sp.scale = d.scale;
     sp.b_layout = d.b_layout;
     sp.valid_len = vl;
+    sp.key_off = key_off;
+    sp.lse = lse;
     sp.ld_a = d.ld_a; sp.ld_b = d.ld_b; sp.ld_d = d.ld_d; sp.ld_e = d.ld_e;
     sp.bs_a = d.bs_a; sp.bs_b = d.bs_b; sp.bs_d = d.bs_d; sp.bs_e = d.bs_e;
     const unsigned grid = (unsigned)(d.batch * d.M);
@@ -727,6 +737,37 @@ mbci_status_t mbci_chain_run(mbci_chain_t h, const void* A, const void* B, const
   if (!h) return fail(MBCI_ERR_INVALID, "handle is NULL");
   DeviceGuard guard(h->device);   // launch on the handle's device, restore the caller's
   return launch(h, A, B, D, E, valid_len, reinterpret_cast<cudaStream_t>(stream));
+}
+
+mbci_status_t mbci_chain_run_partial(mbci_chain_t h, const void* A, const void* B, const void* D, void* E,
+                                     float* lse, const int32_t* valid_len, int64_t key_offset, void* stream) {
+  if (!h) return fail(MBCI_ERR_INVALID, "handle is NULL");
+  if (key_offset < 0 || key_offset > INT32_MAX) return fail(MBCI_ERR_INVALID, "key_offset out of range");
+  if (h->d.op == MBCI_OP_SOFTMAX && !lse && h->d.batch > 0 && h->d.M > 0)
+    return fail(MBCI_ERR_INVALID, "SOFTMAX partial runs need lse");
+  if (h->chain3) return fail(MBCI_ERR_UNSUPPORTED, "split-N partial runs of a three-contraction chain");
+  if (h->d.mask & MBCI_MASK_CAUSAL) return fail(MBCI_ERR_UNSUPPORTED, "split-N partial runs with the causal mask");
+  if (h->plan.kernel == 6) return fail(MBCI_ERR_UNSUPPORTED, "kernel 6 writes no log-sum-exp");
+  DeviceGuard guard(h->device);
+  return launch(h, A, B, D, E, valid_len, reinterpret_cast<cudaStream_t>(stream),
+                h->d.op == MBCI_OP_SOFTMAX ? lse : nullptr, static_cast<int32_t>(key_offset));
+}
+
+mbci_status_t mbci_merge_partials(int32_t parts, const void* E_parts, const float* lse_parts, void* E, int64_t batch,
+                                  int64_t M, int64_t L, int32_t dtype, int32_t op, void* stream) {
+  if (parts < 1 || batch < 0 || M < 0 || L < 0 || dtype < 0 || dtype > 2 || op < 0 || op > 4)
+    return fail(MBCI_ERR_INVALID, "bad merge arguments");
+  if (batch == 0 || M == 0 || L == 0) return MBCI_OK;
+  if (!E_parts || !E || (op == MBCI_OP_SOFTMAX && !lse_parts)) return fail(MBCI_ERR_INVALID, "NULL buffer");
+  const int64_t rows = batch * M;
+  const int64_t es = dtype == 0 ? 4 : 2, ve = 16 / es;
+  const bool vec = L % ve == 0 && aligned16(E_parts) && aligned16(E);
+  int dev = 0, n_sm = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  const cudaError_t e = launch_merge(dtype, E_parts, lse_parts, E, parts, rows, L, op == MBCI_OP_SOFTMAX, vec, n_sm,
+                                     reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "merge kernel launch");
+  return MBCI_OK;
 }
 
 mbci_status_t mbci_chain_run_host(mbci_chain_t h, const void* A, const void* B, const void* D, void* E,

@@ -20,6 +20,8 @@ struct SimtParams {
   const int32_t* valid_len;
   int64_t ld_a, ld_b, ld_d, ld_e;
   int64_t bs_a, bs_b, bs_d, bs_e;
+  int32_t key_off;   // split-N partial runs (as Tc4Params)
+  float* lse;
 };
 
 template <typename T>
@@ -74,7 +76,7 @@ __global__ void __launch_bounds__(kSimtThreads)
   const T* b = B + beta * p.bs_b;
   const T* d = D + beta * p.bs_d;
   int vlen = p.N;
-  if (p.op == 2 && p.valid_len != nullptr) vlen = min(max(p.valid_len[beta], 0), p.N);
+  if (p.op == 2 && p.valid_len != nullptr) vlen = min(max(p.valid_len[beta] - p.key_off, 0), p.N);
   if (p.op == 2 && p.causal) vlen = min(vlen, m + 1);   // key n visible to row m iff n <= m
 
   for (int n = threadIdx.x; n < p.N; n += blockDim.x) {
@@ -99,6 +101,7 @@ __global__ void __launch_bounds__(kSimtThreads)
     }
     sum = block_reduce(sum, false, scratch);
     const float inv = vlen > 0 ? 1.0f / sum : 0.f;
+    if (p.lse != nullptr && threadIdx.x == 0) p.lse[beta * p.M + m] = vlen > 0 ? mx + logf(sum) : -INFINITY;
     for (int n = threadIdx.x; n < p.N; n += blockDim.x) c_row[n] *= inv;
     __syncthreads();
   }

@@ -59,6 +59,10 @@ struct TcParams {
   float scale2;
   uint32_t f_bytes;  // F tile (L rows x TH columns) in SMEM
   uint32_t idesc3;
+  // Split-N partial runs (as Tc4Params): keys [key_off, key_off + N) of the full sequence; SOFTMAX
+  // writes the natural-log row log-sum-exp of that key range to lse[β·M + m] (nullptr: not written).
+  int32_t key_off;
+  float* lse;
 };
 
 // Trace slots (kTraceSlots x u64 per CTA, globaltimer ns unless noted).
@@ -120,7 +124,7 @@ __global__ void __launch_bounds__(kThreads, BN == 64 ? 2 : 1)
   const int h3 = ht * p.TH;                // chain3: F / E columns of this CTA
 
   int n_lim = p.N;
-  if (p.op == 2 && p.valid_len != nullptr) n_lim = min(max(p.valid_len[beta], 0), p.N);
+  if (p.op == 2 && p.valid_len != nullptr) n_lim = min(max(p.valid_len[beta] - p.key_off, 0), p.N);
   // causal (R18): row m sees keys n <= m; the CTA's tiles end at its last row's limit
   const int row_lim = (p.op == 2 && p.causal) ? min(n_lim, m0 + static_cast<int>(threadIdx.x) + 1) : n_lim;
   if (p.op == 2 && p.causal) n_lim = min(n_lim, m0 + 128);
@@ -436,6 +440,8 @@ __global__ void __launch_bounds__(kThreads, BN == 64 ? 2 : 1)
     if (tr && threadIdx.x == 0) tr[kTrEpi] = ptx::globaltimer();
     float inv = (p.op == 2) ? (l_run > 0.f ? 1.0f / l_run : 0.f) : 1.0f;
     const int gm = m0 + row;
+    if (p.lse != nullptr && p.op == 2 && ht == 0 && !p.c3 && gm < p.M)   // one h chunk writes it
+      p.lse[static_cast<int64_t>(beta) * p.M + gm] = l_run > 0.f ? (m_run + log2f(l_run)) * 0.69314718055994531f : -INFINITY;
     uint32_t tOut = tO;
     int outc = TLP, ncols = min(TLP, p.L - h0), ecol0 = h0;
     if (p.c3) {

@@ -78,6 +78,11 @@ struct Tc4Params {
   int32_t pf_bytes;        // kernels 5 / 6: L2 prefetch budget per CTA before the grid-dependency wait
   int32_t dbg;             // diagnostics only (MBCI_T4_DEBUG): 1 = softmax skips its TMEM/math work,
                            // 2 = issuer skips the G2 MMAs, 4 = issuer skips the G1 MMAs
+  // Split-N partial runs (mbci_chain_run_partial): this launch sees keys
+  // [key_off, key_off + N) of the full sequence (valid_len counts full-sequence keys), and, for
+  // SOFTMAX, writes the row log-sum-exp of its key range to lse[β·M + m] (nullptr: not written).
+  int32_t key_off;
+  float* lse;
 };
 
 constexpr int kT4Threads = 512;
@@ -104,8 +109,15 @@ __device__ __forceinline__ uint64_t t4_clk_after(uint32_t dep) {
 
 __device__ __forceinline__ int t4_nlim(const Tc4Params& p, int beta) {
   int n = p.N;
-  if (p.valid_len != nullptr) n = min(max(__ldg(p.valid_len + beta), 0), p.N);
+  if (p.valid_len != nullptr) n = min(max(__ldg(p.valid_len + beta) - p.key_off, 0), p.N);
   return n;
+}
+
+// Split-N partial run: the natural-log row log-sum-exp of this launch's keys, ln 2 · (m + log2 l)
+// with m the running max in log2 units and l the row sum of 2^(z - m); -inf when no key is valid.
+__device__ __forceinline__ void t4_store_lse(const Tc4Params& p, int beta, int gm, float m, float l) {
+  if (p.lse != nullptr && p.op == 2 && gm < p.M)
+    p.lse[static_cast<int64_t>(beta) * p.M + gm] = l > 0.f ? (m + log2f(l)) * 0.69314718055994531f : -INFINITY;
 }
 
 // Key limit of pair unit u for its tile count: key padding and, with the causal mask (DESIGN.md
@@ -631,6 +643,7 @@ __global__ void __launch_bounds__(kT4Threads, 1)
           w1 = l[1] > 0.f ? ptx::ex2(m[1] - mstar) : 0.f;
           const float L = l[0] * w0 + l[1] * w1;
           inv = L > 0.f ? 1.0f / L : 0.f;
+          t4_store_lse(p, beta, gm, mstar, L);
         }
         const uint32_t tO0 = tmem + lane_off + kOCol, tO1 = tO0 + kOStride;
 #pragma unroll 1
@@ -656,17 +669,19 @@ __global__ void __launch_bounds__(kT4Threads, 1)
         T16* erow = reinterpret_cast<T16*>(p.E) + static_cast<int64_t>(beta) * p.bs_e +
                     static_cast<int64_t>(gm) * p.ld_e;
         const uint32_t tO = tmem + lane_off + kOCol + x * kOStride;
-        float l = 0.f;
+        float l = 0.f, mr = 0.f;
         if (nt > 0) {
           ptx::mbar_wait(&o_full[x], ai & 1);
           ptx::tc_fence_after();
           if (tr && x == 0 && row == 0 && ai < 4) tr[490 + 4 * ai] = t4_clk();
           ptx::mbar_wait(&l_full[x], ai & 1);
           l = l_sm[x][ai & 1][row];
+          mr = m_sm[x][ai & 1][row];
           ptx::mbar_arrive(&l_free[x]);
         }
         // whole unit: E = O / l
         const float inv = l > 0.f ? 1.0f / l : 0.f;
+        t4_store_lse(p, beta, gm, mr, l);
 #pragma unroll 1
         for (int c0 = 0; c0 < p.TL; c0 += 16) {
           float v[16];

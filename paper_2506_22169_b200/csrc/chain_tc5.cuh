@@ -482,6 +482,7 @@ __global__ void __launch_bounds__(kT5Threads, 1)
           w1 = l[1] > 0.f ? ptx::ex2(m[1] - mstar) : 0.f;
           const float Lsum = l[0] * w0 + l[1] * w1;
           inv = Lsum > 0.f ? 1.0f / Lsum : 0.f;
+          t4_store_lse(p, beta, m0 + it.half * 128 + row, mstar, Lsum);
         }
         emit(beta, m0 + it.half * 128, 0, w0 * inv, 1, w1 * inv, nt);
         ++ai;
@@ -489,15 +490,17 @@ __global__ void __launch_bounds__(kT5Threads, 1)
       }
 #pragma unroll 1
       for (int x = 0; x < 2; ++x) {
-        float l = 0.f;
+        float l = 0.f, mr = 0.f;
         if (nt > 0) {
           wait_epi(&o_full[x], ai & 1);
           ptx::tc_fence_after();
           if (tr && x == 0 && row == 0 && ai < 4) tr[490 + 4 * ai] = t4_clk();
           wait_epi(&l_full[x], ai & 1);
           l = l_sm[x][ai & 1][row];
+          mr = m_sm[x][ai & 1][row];
           ptx::mbar_arrive(&l_free[x]);
         }
+        t4_store_lse(p, beta, m0 + x * 128 + row, mr, l);
         if (m0 + x * 128 >= p.M) {   // a pair whose second tile is past M: nothing to store
           if (nt > 0) {
             ptx::tc_fence_before();

@@ -40,6 +40,8 @@ struct Tf32Params {
   int64_t ld_a, ld_b, ld_d, ld_e;
   int64_t bs_a, bs_b, bs_d, bs_e;
   uint32_t idesc1, idesc2;   // kind::tf32, K-major A and B; N = 64 (GEMM1), N = TLP (GEMM2)
+  int32_t key_off;           // split-N partial runs (as Tc4Params)
+  float* lse;
 };
 
 constexpr int kTf32Threads = 128;
@@ -160,7 +162,7 @@ __global__ void __launch_bounds__(kTf32Threads, 1)
     ptx::fence_mbar_init();
   }
   int n_lim = p.N;
-  if (p.valid_len != nullptr) n_lim = min(max(__ldg(p.valid_len + beta), 0), p.N);
+  if (p.valid_len != nullptr) n_lim = min(max(__ldg(p.valid_len + beta) - p.key_off, 0), p.N);
   // A tile: rows m0 .. m0 + 127, K-major
   tf32_load_split(sAhi, sAlo, 128, p.KP, A + beta * p.bs_a + static_cast<int64_t>(m0) * p.ld_a, p.M - m0, p.K,
                   p.ld_a, 1, false);
@@ -301,6 +303,9 @@ __global__ void __launch_bounds__(kTf32Threads, 1)
 #pragma unroll
     for (int c = 0; c < kOC; ++c)
       if (c < p.L) e[c] = o[c] * inv;
+    if (p.lse != nullptr && p.op == 2)
+      p.lse[static_cast<int64_t>(beta) * p.M + m0 + row] =
+          l_run > 0.f ? (m_run + log2f(l_run)) * 0.69314718055994531f : -INFINITY;
   }
   ptx::tc_fence_before();
   __syncthreads();

@@ -44,5 +44,8 @@ cudaError_t launch_tf32(bool wide, unsigned grid, cudaStream_t st, const float* 
 const void* simt_fn(int dtype);
 cudaError_t launch_simt(int dtype, unsigned grid, int smem, cudaStream_t st, const void* A, const void* B,
                         const void* D, void* E, const SimtParams& sp);
+// split-N merge (k_merge.cu): E = Σ_r w_r E_r over R packed partials [R][rows][L]; vec = 16-byte chunks
+cudaError_t launch_merge(int dtype, const void* parts, const float* lse, void* E, int R, int64_t rows, int64_t L,
+                         bool softmax, bool vec, int n_sm, cudaStream_t st);
 
 }  // namespace mbci

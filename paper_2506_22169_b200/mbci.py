@@ -105,6 +105,9 @@ class mbci_chain3_desc_t(ctypes.Structure):
                 ("op2", ctypes.c_int32), ("scale2", ctypes.c_float)]
 
 
+_lib.mbci_chain_run_partial.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_int64, _vp]
+_lib.mbci_merge_partials.argtypes = [ctypes.c_int32, _vp, _vp, _vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                     ctypes.c_int32, ctypes.c_int32, _vp]
 _lib.mbci_chain3_create.argtypes = [_P(mbci_chain3_desc_t), ctypes.c_int, _P(_vp)]
 _lib.mbci_chain3_run.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
 
@@ -124,7 +127,8 @@ for _f in ("mbci_chain_create", "mbci_chain_create_with_plan", "mbci_chain_run",
            "mbci_chain_set_trace",
            "mbci_chain_destroy", "mbci_chain_plan", "mbci_chain_describe", "mbci_plan_enumerate",
            "mbci_plan_select", "mbci_model_terms", "mbci_plan_search", "mbci_chain_search_stats",
-           "mbci_chain3_create", "mbci_chain3_run", "mbci_prune_funnel"):
+           "mbci_chain3_create", "mbci_chain3_run", "mbci_prune_funnel",
+           "mbci_chain_run_partial", "mbci_merge_partials"):
     getattr(_lib, _f).restype = _st
 
 EXPORTED = ["mbci_chain_create", "mbci_chain_create_with_plan", "mbci_chain_run", "mbci_chain_run_host",
@@ -132,7 +136,8 @@ EXPORTED = ["mbci_chain_create", "mbci_chain_create_with_plan", "mbci_chain_run"
             "mbci_chain_set_trace",
             "mbci_status_string", "mbci_last_error", "mbci_abi_version", "mbci_hw_default",
             "mbci_plan_enumerate", "mbci_plan_select", "mbci_model_terms", "mbci_plan_search",
-            "mbci_chain_search_stats", "mbci_chain3_create", "mbci_chain3_run", "mbci_prune_funnel"]
+            "mbci_chain_search_stats", "mbci_chain3_create", "mbci_chain3_run", "mbci_prune_funnel",
+            "mbci_chain_run_partial", "mbci_merge_partials"]
 
 # ---- same names as the C ABI ---------------------------------------------------------------
 mbci_chain_create = _lib.mbci_chain_create
@@ -156,6 +161,8 @@ mbci_chain_search_stats = _lib.mbci_chain_search_stats
 mbci_chain3_create = _lib.mbci_chain3_create
 mbci_chain3_run = _lib.mbci_chain3_run
 mbci_prune_funnel = _lib.mbci_prune_funnel
+mbci_chain_run_partial = _lib.mbci_chain_run_partial
+mbci_merge_partials = _lib.mbci_merge_partials
 
 
 def plan_search(desc, measure, hw=None, N=512, n=8, eps=0.01, seed=1, max_rounds=64, model=0):
@@ -237,6 +244,16 @@ def _torch_dtype_code(t):
     return {torch.float32: MBCI_F32, torch.float16: MBCI_F16, torch.bfloat16: MBCI_BF16}[t]
 
 
+def merge_partials(E_parts, lse_parts, E, op="softmax", stream=None):
+    """E_parts [R, batch, M, L], lse_parts [R, batch, M] (fp32), E [batch, M, L]: torch tensors on one device."""
+    import torch
+    R, b, M, L = E_parts.shape
+    s = stream if stream is not None else torch.cuda.current_stream(E.device)
+    check(mbci_merge_partials(R, E_parts.data_ptr(), lse_parts.data_ptr() if lse_parts is not None else None,
+                              E.data_ptr(), b, M, L, _torch_dtype_code(E.dtype),
+                              OPS[op] if isinstance(op, str) else int(op), s.cuda_stream), "mbci_merge_partials")
+
+
 class Chain:
     """Handle wrapper: create once per shape, run many times (torch tensors on the device)."""
 
@@ -281,6 +298,15 @@ class Chain:
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         self.run_ptr(A.data_ptr(), B.data_ptr(), D.data_ptr(), E.data_ptr(),
                      valid_len.data_ptr() if valid_len is not None else 0, s.cuda_stream)
+
+    def run_partial(self, A, B, D, E, lse=None, valid_len=None, key_offset=0, stream=None):
+        """Split-N part over keys [key_offset, key_offset + N): E and (SOFTMAX) lse [batch, M] fp32."""
+        import torch
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        check(mbci_chain_run_partial(self.h, A.data_ptr(), B.data_ptr(), D.data_ptr(), E.data_ptr(),
+                                     lse.data_ptr() if lse is not None else None,
+                                     valid_len.data_ptr() if valid_len is not None else None, key_offset,
+                                     s.cuda_stream), "mbci_chain_run_partial")
 
     def run_host(self, A, B, D, E, valid_len=None, stream=None):
         """End-to-end: host (pinned) torch tensors or numpy arrays in, host E out."""

@@ -77,3 +77,49 @@ def gather_shards(local, counts, group=None):
     out = torch.empty((world * mx,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
     dist.all_gather_into_tensor(out, pad.contiguous(), group=group)
     return torch.cat([out[r * mx: r * mx + counts[r]] for r in range(world)], dim=0)
+
+
+# ---- split-N: the key axis across ranks ------------------------------------
+# A group of `parts` ranks shares the same β range and cuts the keys n into contiguous ranges;
+# each rank runs mbci_chain_run_partial on its range (B, D views at the range's first key, the
+# full-sequence valid_len plus its key offset), the group all-gathers the partial E and the row
+# log-sum-exp over NCCL, and mbci_merge_partials reduces them (the one exchange step of the path).
+
+def key_range(N: int, part: int, parts: int, align: int = 8):
+    """Contiguous [lo, hi) of keys owned by `part` of `parts`; boundaries on multiples of `align`
+    (16-byte TMA offsets for a [K, N] B of 16-bit keys) except the sequence end."""
+    if parts <= 0 or not 0 <= part < parts or align <= 0:
+        raise ValueError("bad part/parts/align")
+    units = -(-N // align)
+    lo_u, hi_u = shard_range(units, part, parts)
+    return min(lo_u * align, N), min(hi_u * align, N)
+
+
+def split_grid(rank: int, world: int, parts: int):
+    """Rank -> (β group, key part) on a (world / parts) x parts grid; ranks of one β group are
+    consecutive, so a group is [g * parts, (g + 1) * parts)."""
+    if parts <= 0 or world % parts != 0 or not 0 <= rank < world:
+        raise ValueError("world must be a multiple of parts")
+    return rank // parts, rank % parts
+
+
+def key_groups(world: int, parts: int):
+    """The rank lists of the β groups (each one key-split group); new_group needs every rank to
+    call it for every group, in the same order."""
+    return [list(range(g * parts, (g + 1) * parts)) for g in range(world // parts)]
+
+
+def gather_partials(E_part, lse_part, group=None):
+    """All-gather a group's partial results: [parts, ...] stacks of E and (SOFTMAX) lse, ordered by
+    group rank (= key range order).  The exchange step of split-N, on the device stream."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return E_part.unsqueeze(0), (lse_part.unsqueeze(0) if lse_part is not None else None)
+    w = dist.get_world_size(group)
+
+    def gather(x):   # concatenated along dim 0 (what every backend accepts), viewed as [w, ...]
+        out = torch.empty((w * x.shape[0],) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
+        dist.all_gather_into_tensor(out, x.contiguous(), group=group)
+        return out.view((w,) + tuple(x.shape))
+    return gather(E_part), (gather(lse_part) if lse_part is not None else None)

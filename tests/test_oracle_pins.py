@@ -462,3 +462,45 @@ def test_funnel_limits_and_ragged_dims():
     keep = [t for t in model.tile_options(1000) if not model.rule3_reject(1000, t)]
     assert keep == [t for t in range(16, 1009, 16) if math.ceil(1000 / t) * t - 1000 < 50]
     assert 1008 in model.tile_options(1000) and 1008 in keep   # 8 / 1000 padding
+
+
+# ---- split-N statistic: the row log-sum-exp -----------------------------------
+def test_row_lse_against_scipy_logsumexp():
+    from split_util import slice_keys  # noqa: F401
+    inp = gen.make_chain_inputs(11, "bf16", 3, 9, 21, 16, 8, 1, valid_len_range=(0, 21))
+    A, B, _ = _f64(inp)
+    s = 0.37
+    z = s * np.einsum("bmk,bkn->bmn", A, _bmat(inp, B))
+    for vl in (None, inp.valid_len):
+        got = oracle.row_lse(inp, s, vl)
+        for b in range(inp.batch):
+            v = inp.N if vl is None else int(vl[b])
+            ref = scipy.special.logsumexp(z[b, :, :v], axis=1) if v > 0 else np.full(inp.M, -np.inf)
+            assert np.allclose(got[b], ref, rtol=0, atol=1e-12) or (v == 0 and np.all(got[b] == -np.inf))
+    # one valid key: lse = s * C[m, 0] exactly; no valid key: -inf
+    got = oracle.row_lse(inp, s, np.array([1, 0, 21], dtype=np.int32))
+    assert np.allclose(got[0], z[0, :, 0], rtol=0, atol=1e-12)
+    assert np.all(got[1] == -np.inf)
+
+
+@pytest.mark.parametrize("cuts", [(0, 7, 21), (0, 1, 2, 21), (0, 20, 21), (0, 8, 16, 21)])
+@pytest.mark.parametrize("masked", [False, True])
+def test_split_n_combination_reproduces_full_chain(cuts, masked):
+    """Partial chains over key ranges, combined by log-sum-exp weights, equal the full chain: the
+    identity the GPU merge (mbci_merge_partials) implements, checked on the oracle alone."""
+    from split_util import local_valid, lse_combine, slice_keys
+    inp = gen.make_chain_inputs(12, "f16", 4, 10, 21, 16, 12, 1, valid_len_range=(0, 21) if masked else None)
+    vl = inp.valid_len if masked else None
+    s = 0.25
+    full = oracle.chain(inp, "softmax", s, vl)
+    parts, lses = [], []
+    for n0, n1 in zip(cuts, cuts[1:]):
+        sub = slice_keys(inp, n0, n1)
+        v = local_valid(vl, n0, n1)
+        parts.append(oracle.chain(sub, "softmax", s, v))
+        lses.append(oracle.row_lse(sub, s, v))
+    assert np.allclose(lse_combine(parts, lses), full, rtol=0, atol=1e-12)
+    # linear ops: the partial products simply add up
+    full_none = oracle.chain(inp, "none", 1.0)
+    parts = [oracle.chain(slice_keys(inp, a, b), "none", 1.0) for a, b in zip(cuts, cuts[1:])]
+    assert np.allclose(np.sum(parts, axis=0), full_none, rtol=0, atol=1e-10)
