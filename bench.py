@@ -326,23 +326,27 @@ def run_cuda(args, rank, world, local_rank):
         with torch.cuda.stream(stream):
             g.replay()
         stream.synchronize()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    ev0.record(stream)
-    with torch.cuda.stream(stream):
-        g.replay()
-    ev1.record(stream)
-    ev1.synchronize()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    # the timed region: the K-step graph replayed `repeats` times, each bracketed by CUDA events on
+    # the launch stream (barrier + synchronize on both sides); value = the median replay, max over ranks
+    reps_ms = []
+    for _ in range(max(1, args.repeats)):
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        with torch.cuda.stream(stream):
+            g.replay()
+        ev1.record(stream)
+        ev1.synchronize()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        reps_ms.append(sharding.max_over_ranks(ev0.elapsed_time(ev1)))
     t_load1 = time.time()
     time.sleep(0.25)
     sampler.stop()
-    ms_local = ev0.elapsed_time(ev1)
-    ms = sharding.max_over_ranks(ms_local)
+    ms = statistics.median(reps_ms)
     ms_per_step = ms / args.steps
     total_bytes = sharding.sum_over_ranks(step_bytes)
     gbs = total_bytes / (ms_per_step * 1e-3) / 1e9
@@ -410,7 +414,9 @@ def run_cuda(args, rank, world, local_rank):
         "config": {"workload": desc, "name": name, "batch_heads_per_gpu": nb, "global_batch_heads": global_b,
                    "M": M, "N": N, "K": K, "L": L, "op": op, "scale": sc, "b_layout": b_layout,
                    "l2": f"{rot} rotating input sets ({rot * step_bytes / 2**20:.0f} MiB) > 2x L2 between reuses",
-                   "timing": "K steps in one CUDA graph, CUDA events on the launch stream, max over ranks",
+                   "timing": f"K steps in one CUDA graph, CUDA events on the launch stream, max over ranks, "
+                             f"median of {len(reps_ms)} replays",
+                   "replay_us_per_step": [round(x / args.steps * 1e3, 3) for x in reps_ms],
                    "parallelism": f"dp{world} (batch x head sharding, no data-path collective)",
                    "plan": ch.describe(), "env": {k: v for k, v in os.environ.items() if k.startswith("MBCI_")}},
         "hbm_frac_of_8TBps": gbs / (8000.0 * world),
@@ -418,7 +424,7 @@ def run_cuda(args, rank, world, local_rank):
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_gbs, "unit": "GB/s", "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "api": "mbci_chain_run_host", "gpu_local_cpus": numa},
-        "gpu_launches": launches * args.steps,
+        "gpu_launches": launches * args.steps, "timed_replays": len(reps_ms),
         "clocks": clocks,
         "gather_check": gcheck,
     }
@@ -631,6 +637,7 @@ def main():
     ap.add_argument("--sustain", type=float, default=1.0, help="seconds of untimed load for the clock sampler")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--repeats", type=int, default=5, help="timed replays of the K-step graph (median reported)")
     ap.add_argument("--split-n", type=int, default=1,
                     help="cut the key axis into P ranges (SURVEY f1): groups of P ranks all-gather and merge")
     args = ap.parse_args()

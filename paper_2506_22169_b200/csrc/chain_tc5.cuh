@@ -20,6 +20,8 @@
 // One tcgen05 issuer thread per slot (warps 12 and 14), each in its own order, per step g:
 //     wait s_free(x, g) -> G1(x, g + 1) -> commit s_full(x)
 //     wait p_full(x, g) -> G2(x, g)     -> commit p_free(x) [+ kv_empty, o_full]
+// (flags bit 8, the default: event-driven — both hand-offs polled, G1 and G2 issued in whichever
+// order their inputs complete, so a late K tile no longer holds back the G2 the softmax waits on)
 // so neither slot's next score tile waits behind the other slot's hand-offs (a single issuer
 // serialising both slots cost ~0.45 us per step on C2: it blocked on the full MMA issue queue
 // after each G2 before it could issue the other slot's G1).  Deadlock-free: every wait is for
@@ -96,6 +98,27 @@ __device__ __forceinline__ void t5_exp_row(uint32_t (&pk)[64], const uint32_t (&
     }
     if (bar != 0 && ch == arrive_after) ptx::named_bar_arrive(bar, 64);
   }
+}
+
+// NONE / SCALE / RELU / GELU: the packed 16-bit row of op(s·S) into registers (the caller stores it
+// once G2 of the previous step has released P_x)
+template <bool BF16, bool ACT>
+__device__ __forceinline__ void t5_cvt_row_impl(uint32_t (&pk)[64], const uint32_t (&sr)[kT4BN], float sc, int op) {
+  const float2 sc2 = make_float2(sc, sc);
+#pragma unroll
+  for (int cp = 0; cp < 64; ++cp) {
+    float2 z = __fmul2_rn(make_float2(__uint_as_float(sr[2 * cp]), __uint_as_float(sr[2 * cp + 1])), sc2);
+    if constexpr (ACT) {
+      z.x = ptx::act(op, z.x);
+      z.y = ptx::act(op, z.y);
+    }
+    pk[cp] = ptx::pack2<BF16>(z.x, z.y);
+  }
+}
+template <bool BF16>
+__device__ __forceinline__ void t5_cvt_row(uint32_t (&pk)[64], const uint32_t (&sr)[kT4BN], float sc, int op) {
+  if (op >= 3) t5_cvt_row_impl<BF16, true>(pk, sr, sc, op);   // one uniform branch per tile
+  else t5_cvt_row_impl<BF16, false>(pk, sr, sc, op);
 }
 
 // P_x <- the packed row (64 columns of 16-bit pairs), 16 columns per tcgen05.st
@@ -322,13 +345,15 @@ __global__ void __launch_bounds__(kT5Threads, 1)
         T4Cursor c1, c2;   // c1: step of the next G1 (one ahead of c2), c2: step of the next G2
         c1.init(p, G);
         c2 = c1;
-        // G1(x) of step c1: S_x = Q_x · K_(tile of slot x)
-        auto issue_g1 = [&]() {
-          if (c1.j == 0) wait1(&q_full[c1.qb], c1.qph);
+        // G1(x) of step c1: S_x = Q_x · K_(tile of slot x)  (ready: its inputs were tested already)
+        auto issue_g1 = [&](bool ready = false) {
           int kst;
           uint32_t kph;
           c1.entry(x, S, kst, kph);
-          wait1(&kv_full[kst], kph);
+          if (!ready) {
+            if (c1.j == 0) wait1(&q_full[c1.qb], c1.qph);
+            wait1(&kv_full[kst], kph);
+          }
           ptx::tc_fence_after();
           const uint32_t q_lo = (sQ0 + (c1.qb * 2 + (c1.hf ? 0 : x)) * p.q_bytes) >> 4;   // half: one Q tile
           const uint32_t k_lo = (sKV0 + kst * kv_stage) >> 4;
@@ -360,6 +385,74 @@ __global__ void __launch_bounds__(kT5Threads, 1)
           c2.valid = false;
         }
         if (c1.valid) issue_g1();
+        // G2(x) of step c2: O_x += P_x · V_(tile of slot x)  (its inputs are complete)
+        auto issue_g2 = [&]() {
+          if (tr && c2.g < kT4TrTiles) tr[T4TR(c2.g, 10 + x)] = t4_clk();
+          ptx::tc_fence_after();
+          int vst;
+          uint32_t vph;
+          c2.entry(x, S, vst, vph);
+          const uint32_t v_lo = (sKV0 + vst * kv_stage + p.b_stage_bytes) >> 4;
+          const uint32_t acc0 = c2.j > 0 ? 1u : 0u;
+#pragma unroll
+          for (int ks = 0; ks < kT4BN / 16; ++ks)
+            if (!(dbg & 2)) ptx::mma_ts(tO, tP + ks * 8, dD + v_lo + ks * 128, idesc2, ks > 0 ? 1u : acc0);
+          ptx::mma_commit(&p_free[x]);
+          if (tr && c2.g < kT4TrTiles) tr[T4TR(c2.g, 12 + x)] = t4_clk();
+          ptx::mma_commit(&kv_empty[vst]);
+          if (c2.hf) ptx::mma_commit(&kv_empty[vst]);
+          if (c2.j == c2.nt - 1) ptx::mma_commit(&o_full[x]);
+          c2.advance(p, G);
+        };
+        if (p.flags & 256) {
+          // Event-driven order (flags bit 8): poll both hand-offs and issue G2(c2) as soon as P_x is
+          // written and G1(c1) as soon as S_x is free and its K tile has landed, whichever comes
+          // first, so a late K tile no longer holds back the G2 the softmax waits on (p_free).
+          // Phases stay unambiguous: G1(c1) needs s_free of step c1 - 1, which the softmax only
+          // arrives after S(c1 - 1) exists; G2(c2) needs p_full of step c2 < c1.
+          const uint64_t t0 = ptx::globaltimer();
+          uint32_t idle = 0;
+          while (c2.valid) {
+            bool did = false;
+            if (c1.valid && ptx::mbar_test(&s_free[x], (c1.g - 1) & 1) &&
+                (c1.j != 0 || ptx::mbar_test(&q_full[c1.qb], c1.qph))) {
+              int kst;
+              uint32_t kph;
+              c1.entry(x, S, kst, kph);
+              if (ptx::mbar_test(&kv_full[kst], kph)) {
+                issue_g1(true);
+                did = true;
+              }
+            }
+            if (c2.g < c1.g && ptx::mbar_test(&p_full[x], c2.g & 1) &&
+                (c2.j != 0 || c2.ai == 0 || ptx::mbar_test(&o_free[x], (c2.ai - 1) & 1))) {
+              issue_g2();
+              did = true;
+            }
+            if (!did) {
+              // sleep (suspend-time hint) on the first unmet input in the softmax's own order — S_x
+              // free comes before P_x written — then re-test both
+              uint64_t* bar;
+              uint32_t par;
+              if (c1.valid && !ptx::mbar_test(&s_free[x], (c1.g - 1) & 1)) {
+                bar = &s_free[x];
+                par = (c1.g - 1) & 1;
+              } else if (c1.valid && c1.j == 0 && !ptx::mbar_test(&q_full[c1.qb], c1.qph)) {
+                bar = &q_full[c1.qb];
+                par = c1.qph;
+              } else if (c2.g < c1.g) {
+                bar = &p_full[x];
+                par = c2.g & 1;
+              } else {
+                int kst;
+                c1.entry(x, S, kst, par);
+                bar = &kv_full[kst];
+              }
+              ptx::mbar_try_wait_hint(ptx::smem_u32(bar), par, 100);
+              if (((++idle) & 1023u) == 0 && ptx::globaltimer() - t0 > 4000000000ull) __trap();
+            }
+          }
+        }
         uint32_t ph = 0;   // parity of step c2.g (s_free / p_full phases count this slot's steps)
         while (c2.valid) {
           if (c1.valid) {
@@ -565,9 +658,17 @@ __global__ void __launch_bounds__(kT5Threads, 1)
         if (lane0) ptx::mbar_arrive(&s_free[x]);   // S_x may be overwritten by G1(x, g + 1)
         if (p.op != 2) {
           // NONE / SCALE: padded keys have S = 0 and zero V rows (TMA fill), no masking needed
-          if (g > 0) ptx::mbar_wait(&p_free[x], ph ^ 1u);   // G2_x(g - 1) has read P_x
-          ptx::tc_fence_after();
-          t4_cvt_row<BF16>(tP, sr, sc, p.op);
+          if (p.flags & 512) {   // convert first, then wait for G2_x(g - 1) to release P_x
+            uint32_t pk[64];
+            t5_cvt_row<BF16>(pk, sr, sc, p.op);
+            if (g > 0) ptx::mbar_wait(&p_free[x], ph ^ 1u);
+            ptx::tc_fence_after();
+            t5_store_p(tP, pk);
+          } else {
+            if (g > 0) ptx::mbar_wait(&p_free[x], ph ^ 1u);   // G2_x(g - 1) has read P_x
+            ptx::tc_fence_after();
+            t4_cvt_row<BF16>(tP, sr, sc, p.op);
+          }
         } else {
           float mx;
           if (full)

@@ -183,9 +183,16 @@ static void score_b200(const mbci_chain_desc_t& d, const mbci_hw_t& hw, mbci_pla
     // (round 2, profiles/r2_k5_k6_prefetch_ab.txt): it ranks just behind kernel 5
     if (p.kernel == 6) t_pair *= 1.001;
     const double fixed = p.kernel >= 5 ? 2.0e-6 : 3.0e-6;
-    // (ties go to the deeper ring, up to the 4 stages that keep two Q buffers at d = 64)
+    // Ties go to the deeper ring: softmax up to the 4 stages that keep two Q buffers at d = 64;
+    // the linear ops (long items, no exponentials) to the deepest ring that still keeps two Q
+    // buffers (kernel 5 on C4 K = L = 16: 4 -> 7 stages 44.8 -> 43.0 us, profiles/r2_k5_ring_sweep.txt).
+    int32_t pref = std::min<int32_t>(p.stages, 4);
+    if (p.kernel >= 5 && d.op != MBCI_OP_SOFTMAX) {
+      Tc4Layout lay;
+      pref = (tc5_layout(p.TK / 16, p.TL, p.stages, d.b_layout, &lay, hw.smem_max) && lay.q_bufs == 2) ? p.stages : 0;
+    }
     p.t_b200 = std::max(t_hbm, static_cast<double>(rounds * ntm + tail_tiles) * t_pair) + fixed -
-               1e-12 * std::min<int32_t>(p.stages, 4) + (p.kernel == 6 ? 1e-9 : 0.0);
+               1e-12 * pref + (p.kernel == 6 ? 1e-9 : 0.0);
     return;
   }
   int32_t occ = 1;
