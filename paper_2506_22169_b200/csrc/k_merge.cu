@@ -62,7 +62,10 @@ __device__ __forceinline__ void mg_row_stats(const float* lse, int64_t rows, int
   inv = sum > 0.f ? 1.0f / sum : 0.f;
 }
 
-// vector variant: VE elements (16 bytes) per thread-chunk
+// vector variant: VE elements (16 bytes) per thread-chunk, R <= kMergeRMax parts.  Every load of a
+// chunk (the R lse values of its row and the R 16-byte partial chunks) is issued before any is
+// used, so a thread keeps R + R/4 independent requests in flight instead of a dependent chain.
+constexpr int kMergeRMax = 8;
 template <typename T>
 __global__ void __launch_bounds__(256) k_merge_vec(const T* __restrict__ parts, const float* __restrict__ lse,
                                                    T* __restrict__ E, int R, int64_t rows, int64_t L, int softmax) {
@@ -71,22 +74,43 @@ __global__ void __launch_bounds__(256) k_merge_vec(const T* __restrict__ parts, 
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t row = i / chunks, c0 = (i - row * chunks) * VE;
-    float mstar = 0.f, inv = 1.f;
-    if (softmax) mg_row_stats(lse, rows, R, row, mstar, inv);
+    uint4 v[kMergeRMax];
+    float l[kMergeRMax];
+#pragma unroll
+    for (int r = 0; r < kMergeRMax; ++r) {
+      if (r < R) {
+        v[r] = __ldg(reinterpret_cast<const uint4*>(parts + r * part_stride + row * L + c0));
+        l[r] = softmax ? __ldg(lse + static_cast<int64_t>(r) * rows + row) : 0.f;
+      }
+    }
+    float w[kMergeRMax];
+    float mstar = -INFINITY, sum = 0.f;
+#pragma unroll
+    for (int r = 0; r < kMergeRMax; ++r)
+      if (r < R) mstar = fmaxf(mstar, l[r]);
+#pragma unroll
+    for (int r = 0; r < kMergeRMax; ++r) {
+      if (r < R) {
+        w[r] = !softmax ? 1.f : (l[r] == -INFINITY ? 0.f : __expf(l[r] - mstar));
+        sum += w[r];
+      }
+    }
+    const float inv = !softmax ? 1.f : (sum > 0.f ? 1.0f / sum : 0.f);
     float acc[VE];
 #pragma unroll
     for (int q = 0; q < VE; ++q) acc[q] = 0.f;
-    for (int r = 0; r < R; ++r) {
-      const float w = mg_weight(lse, rows, R, row, r, softmax != 0, mstar, inv);
-      const uint4 v = __ldg(reinterpret_cast<const uint4*>(parts + r * part_stride + row * L + c0));
-      const T* t = reinterpret_cast<const T*>(&v);
 #pragma unroll
-      for (int q = 0; q < VE; ++q) acc[q] = fmaf(w, mg_f(t[q]), acc[q]);
+    for (int r = 0; r < kMergeRMax; ++r) {
+      if (r < R) {
+        const T* t = reinterpret_cast<const T*>(&v[r]);
+#pragma unroll
+        for (int q = 0; q < VE; ++q) acc[q] = fmaf(w[r], mg_f(t[q]), acc[q]);
+      }
     }
     uint4 o;
     T* ot = reinterpret_cast<T*>(&o);
 #pragma unroll
-    for (int q = 0; q < VE; ++q) ot[q] = mg_from<T>(acc[q]);
+    for (int q = 0; q < VE; ++q) ot[q] = mg_from<T>(acc[q] * inv);
     *reinterpret_cast<uint4*>(E + row * L + c0) = o;
   }
 }
@@ -111,9 +135,10 @@ template <typename T>
 cudaError_t merge_t(const void* parts, const float* lse, void* E, int R, int64_t rows, int64_t L, bool softmax,
                     bool vec, int n_sm, cudaStream_t st) {
   constexpr int VE = 16 / sizeof(T);
+  vec = vec && R <= kMergeRMax;
   const int64_t work = vec ? rows * (L / VE) : rows * L;
-  const int64_t blocks = (work + 255) / 256;
-  const unsigned grid = static_cast<unsigned>(blocks < 8LL * n_sm ? (blocks > 0 ? blocks : 1) : 8LL * n_sm);
+  const int64_t blocks = (work + 255) / 256;   // one chunk per thread up to 64 blocks per SM
+  const unsigned grid = static_cast<unsigned>(blocks < 64LL * n_sm ? (blocks > 0 ? blocks : 1) : 64LL * n_sm);
   if (vec)
     k_merge_vec<T><<<grid, 256, 0, st>>>(static_cast<const T*>(parts), lse, static_cast<T*>(E), R, rows, L,
                                          softmax ? 1 : 0);

@@ -258,3 +258,13 @@ def test_prune_funnel_errors(m):
     f = m.mbci_funnel_t()
     assert m.mbci_prune_funnel(0, 1, 1, 1, 2, 1000, ctypes.byref(f)) == 1
     assert m.mbci_prune_funnel(16, 16, 16, 16, 2, 1000, None) == 1
+
+
+def test_linear_ops_prefer_deepest_ring_with_two_q_buffers(m):
+    """Kernel 5 on plain chains: the deepest K/V ring that keeps both Q buffers (C4 K = L = 16: 7
+    stages, measured 44.8 -> 43.0 us vs 4); softmax keeps 4 stages (short items need two Q buffers)."""
+    for (K, L, op, st) in [(16, 16, "none", 7), (32, 32, "none", 5), (64, 64, "none", 4), (64, 64, "softmax", 4)]:
+        d = m.make_desc(64, 2048, 2048, K, L, "bf16", op, 0.125, b_layout=0 if op == "none" else 1)
+        p = m.mbci_plan_t()
+        m.check(m.mbci_plan_select(d, None, p))
+        assert p.kernel == 5 and p.stages == st, (K, L, op, p.kernel, p.stages)
