@@ -40,14 +40,17 @@ def stale_lib(lib) -> bool:
     return any(os.path.getmtime(p) > t for p in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False, trace: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, trace: bool = False, variant: str = "",
+          defines=()) -> str:
     """libmbci.so (production) or, with trace=True, libmbci_trace.so (per-CTA event timestamps
-    compiled in; loaded by the binding when MBCI_LIB=trace — diagnostics only)."""
-    lib = LIB_TRACE if trace else LIB
+    compiled in; loaded by the binding when MBCI_LIB=trace — diagnostics only).  variant + defines:
+    an A/B copy libmbci_<variant>.so compiled with -D<defines> (MBCI_LIB=ab:libmbci_<variant>.so)."""
+    lib = LIB_TRACE if trace else (os.path.join(HERE, f"libmbci_{variant}.so") if variant else LIB)
     if force or stale_lib(lib):
-        extra = ["-DMBCI_TRACE=1"] if trace else []
+        extra = (["-DMBCI_TRACE=1"] if trace else []) + [f"-D{d}" for d in defines]
         # objects outside the repo: only the linked .so travels to the GPU box
-        objdir = os.path.join(tempfile.gettempdir(), "mbci_build", "trace" if trace else "release")
+        objdir = os.path.join(tempfile.gettempdir(), "mbci_build",
+                              "trace" if trace else (variant or "release"))
         os.makedirs(objdir, exist_ok=True)
         objs, procs = [], []
         for src in SOURCES:
