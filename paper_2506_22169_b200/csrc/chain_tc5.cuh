@@ -488,7 +488,9 @@ __global__ void __launch_bounds__(kT5Threads, 1)
     ptx::setmaxnreg_dec<80>();
     // flags bit 7: the epilogue sleeps in its waits (suspend-time hint) to free issue slots
     auto wait_epi = [&](uint64_t* bar, uint32_t parity) {
-      if (p.flags & 128) ptx::mbar_wait_lazy(bar, parity); else ptx::mbar_wait(bar, parity);
+      if (p.flags & 1024) ptx::mbar_wait_backoff(bar, parity);   // bit 10: sleep between polls
+      else if (p.flags & 128) ptx::mbar_wait_lazy(bar, parity);
+      else ptx::mbar_wait(bar, parity);
     };
     const int row = threadIdx.x - 256;   // TMEM lane (warp 8+w reads lanes 32w..32w+31)
     const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;

@@ -131,6 +131,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     if (((++spins) & 1023u) == 0 && globaltimer() - t0 > 4000000000ull) __trap();
   }
 }
+// Long waits of latency-tolerant roles (the epilogue waits a whole item for O): try_wait, then
+// sleep with exponential backoff up to cap_ns between polls, so the waiting warp leaves its
+// SMSP's issue slots to the softmax warp it shares them with.
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity, uint32_t cap_ns = 128) {
+  const uint32_t addr = smem_u32(bar);
+  if (mbar_try_wait(addr, parity)) return;
+  const uint64_t t0 = globaltimer();
+  uint32_t ns = 16;
+  for (uint32_t n = 0;; ++n) {
+    __nanosleep(ns);
+    if (mbar_try_wait(addr, parity)) return;
+    if (ns < cap_ns) ns <<= 1;
+    if ((n & 255u) == 255u && globaltimer() - t0 > 4000000000ull) __trap();
+  }
+}
 
 template <uint32_t N>
 __device__ __forceinline__ void setmaxnreg_inc() {

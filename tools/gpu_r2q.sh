@@ -1,0 +1,8 @@
+#!/bin/bash
+run() { env $3 timeout 300 python bench.py --config $1 --steps 100 --warmup 5 --repeats 5 --sustain 0.3 --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.readline()); print('$1 $2', round(d['ms_per_step']*1000,2), 'us', d['clocks']['sm_mhz'], d['clocks']['reasons'])"; }
+for rep in 1 2; do for c in C2 C6 C4-16; do
+  run $c "old-wait 785" "MBCI_T5_FLAGS=785 MBCI_LIB=ab:libmbci_oldwait.so"
+  run $c "old-wait 1809" "MBCI_T5_FLAGS=1809 MBCI_LIB=ab:libmbci_oldwait.so"
+  run $c "new-wait 785" "MBCI_T5_FLAGS=785"
+  run $c "new-wait 1809" "MBCI_T5_FLAGS=1809"
+done; done
