@@ -448,7 +448,7 @@ __global__ void __launch_bounds__(kT5Threads, 1)
                 c1.entry(x, S, kst, par);
                 bar = &kv_full[kst];
               }
-              ptx::mbar_try_wait_hint(ptx::smem_u32(bar), par, 100);
+              if (!(p.flags & 4)) ptx::mbar_try_wait_hint(ptx::smem_u32(bar), par, 100);   // bit 2: pure polling
               if (((++idle) & 1023u) == 0 && ptx::globaltimer() - t0 > 4000000000ull) __trap();
             }
           }
@@ -623,6 +623,12 @@ __global__ void __launch_bounds__(kT5Threads, 1)
     // Exp-phase turns (flags bit 0, softmax only): named barriers 1-4 = slot 0's turn on SMSP q,
     // 5-8 = slot 1's; slot 0 goes first.
     const bool turns = (p.flags & 1) != 0 && p.op == 2;
+    // flags bit 11: on SOFTMAX the softmax warps poll s_full / p_free with test_wait instead of
+    // try_wait (C2 -1.3 %; on the linear ops polling costs 7 %, so they keep try_wait)
+    const bool sm_spin = (p.flags & 2048) != 0 && p.op == 2;
+    auto wait_sm = [&](uint64_t* bar, uint32_t parity) {
+      if (sm_spin) ptx::mbar_spin(bar, parity); else ptx::mbar_wait(bar, parity);
+    };
     const uint32_t bar_mine = 1 + (warp & 3) + 4 * x, bar_other = 1 + (warp & 3) + 4 * (1 - x);
     const int turn_chunk = 3 - ((p.flags >> 4) & 3);   // flags bits 4-5: hand over 0-3 chunks early
     int g = 0, ai = 0;
@@ -638,13 +644,13 @@ __global__ void __launch_bounds__(kT5Threads, 1)
       float2 l2 = make_float2(0.f, 0.f), l2b = make_float2(0.f, 0.f);
       for (int j = 0; j < nt; ++j, ++g) {
         const uint32_t ph = g & 1;
-        if (!(dbg & 128)) ptx::mbar_wait(&s_full[x], ph);   // 128: free-running softmax (timing only)
+        if (!(dbg & 128)) wait_sm(&s_full[x], ph);   // 128: free-running softmax (timing only)
         ptx::tc_fence_after();
         if (tr && row == 0 && g < kT4TrTiles) tr[T4TR(g, x)] = t4_clk();
         if (dbg & 1) {   // barrier protocol only
           __syncwarp();
           if (lane0) ptx::mbar_arrive(&s_free[x]);
-          if (g > 0) ptx::mbar_wait(&p_free[x], ph ^ 1u);
+          if (g > 0) wait_sm(&p_free[x], ph ^ 1u);
           __syncwarp();
           if (lane0) ptx::mbar_arrive(&p_full[x]);
           continue;
@@ -663,11 +669,11 @@ __global__ void __launch_bounds__(kT5Threads, 1)
           if (p.flags & 512) {   // convert first, then wait for G2_x(g - 1) to release P_x
             uint32_t pk[64];
             t5_cvt_row<BF16>(pk, sr, sc, p.op);
-            if (g > 0) ptx::mbar_wait(&p_free[x], ph ^ 1u);
+            if (g > 0) wait_sm(&p_free[x], ph ^ 1u);
             ptx::tc_fence_after();
             t5_store_p(tP, pk);
           } else {
-            if (g > 0) ptx::mbar_wait(&p_free[x], ph ^ 1u);   // G2_x(g - 1) has read P_x
+            if (g > 0) wait_sm(&p_free[x], ph ^ 1u);   // G2_x(g - 1) has read P_x
             ptx::tc_fence_after();
             t4_cvt_row<BF16>(tP, sr, sc, p.op);
           }
@@ -684,7 +690,7 @@ __global__ void __launch_bounds__(kT5Threads, 1)
           // the early wait, for A/B measurements).
           bool p_ready = g == 0;
           if (!p_ready && (p.flags & 8)) {
-            if (!(dbg & 128)) ptx::mbar_wait(&p_free[x], ph ^ 1u);
+            if (!(dbg & 128)) wait_sm(&p_free[x], ph ^ 1u);
             ptx::tc_fence_after();
             p_ready = true;
           }
@@ -693,7 +699,7 @@ __global__ void __launch_bounds__(kT5Threads, 1)
           } else if (__any_sync(0xffffffffu, m_tile > m_run + kT4Tau)) {
             // warp-uniform (tcgen05.ld/st are warp-collective); O_x must hold G2_x(g - 1)
             if (!p_ready) {
-              if (!(dbg & 128)) ptx::mbar_wait(&p_free[x], ph ^ 1u);
+              if (!(dbg & 128)) wait_sm(&p_free[x], ph ^ 1u);
               ptx::tc_fence_after();
               p_ready = true;
             }
@@ -723,7 +729,7 @@ __global__ void __launch_bounds__(kT5Threads, 1)
             t5_exp_row<BF16, 0, true>(pk, sr, sc, m_run, valid, l2, l2b, turn_chunk, turns ? bar_other : 0u);
           if (tr && row == 0 && g < kT4TrTiles) tr[T4TR(g, 6 + x)] = t4_clk();   // exps done
           if (!p_ready) {
-            if (!(dbg & 128)) ptx::mbar_wait(&p_free[x], ph ^ 1u);
+            if (!(dbg & 128)) wait_sm(&p_free[x], ph ^ 1u);
             ptx::tc_fence_after();
           }
           t5_store_p(tP, pk);
