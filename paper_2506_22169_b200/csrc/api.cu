@@ -98,6 +98,13 @@ int t5_flags_default() {
                 // bit 11: softmax warps poll s_full / p_free with test_wait on SOFTMAX (~1 %)
 }
 
+// Kernel-4 feature flags (MBCI_T4_FLAGS overrides): bit 10 the epilogue sleeps between polls.
+int t4_flags_default() {
+  const char* e = getenv("MBCI_T4_FLAGS");
+  if (e) return atoi(e) & 0x400;
+  return 0;
+}
+
 // Kernel-6 feature flags (MBCI_T6_FLAGS overrides): bit 0 exp-phase turns between the slots,
 // bit 4 hand the turn over one 16-pair chunk early, bit 2 spinning single-thread waits.
 int t6_flags_default() {
@@ -328,7 +335,7 @@ mbci_status_t setup_plan(mbci_chain* h) {
     t.items = (int32_t)(halves ? t.half_from + 2 * rem : units);
     h->grid2 = (int32_t)std::max<int64_t>(1, std::min<int64_t>(n_sm, t.items));
     p.n_block = t.items;
-    t.flags = p.kernel == 5 ? t5_flags_default() : (p.kernel == 6 ? t6_flags_default() : 0);
+    t.flags = p.kernel == 5 ? t5_flags_default() : (p.kernel == 6 ? t6_flags_default() : t4_flags_default());
     t.pf_bytes = p.kernel >= 5 ? pf_bytes_default() : 0;
     t.burst = (p.kernel >= 5 && !env_is("MBCI_T5_BURST", "0")) ? 1 : 0;
     h->threads = p.kernel == 6 ? kT6Threads : (p.kernel == 5 ? kT5Threads : kT4Threads);

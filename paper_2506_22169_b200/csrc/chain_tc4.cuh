@@ -598,6 +598,10 @@ __global__ void __launch_bounds__(kT4Threads, 1)
     const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
     using T16 = uint16_t;
     int ai = 0;
+    // flags bit 10 (MBCI_T4_FLAGS): the epilogue sleeps between polls of its long O waits
+    auto wait_epi = [&](uint64_t* bar, uint32_t parity) {
+      if (p.flags & 1024) ptx::mbar_wait_backoff(bar, parity); else ptx::mbar_wait(bar, parity);
+    };
     auto store_row = [&](T16* erow, int gm, int c0, const float* v, float inv) {
       uint32_t w[8];
 #pragma unroll
@@ -629,8 +633,8 @@ __global__ void __launch_bounds__(kT4Threads, 1)
         float l[2], m[2];
 #pragma unroll
         for (int x = 0; x < 2; ++x) {
-          ptx::mbar_wait(&o_full[x], ai & 1);
-          ptx::mbar_wait(&l_full[x], ai & 1);
+          wait_epi(&o_full[x], ai & 1);
+          wait_epi(&l_full[x], ai & 1);
           l[x] = l_sm[x][ai & 1][row];
           m[x] = m_sm[x][ai & 1][row];
           ptx::mbar_arrive(&l_free[x]);
@@ -671,10 +675,10 @@ __global__ void __launch_bounds__(kT4Threads, 1)
         const uint32_t tO = tmem + lane_off + kOCol + x * kOStride;
         float l = 0.f, mr = 0.f;
         if (nt > 0) {
-          ptx::mbar_wait(&o_full[x], ai & 1);
+          wait_epi(&o_full[x], ai & 1);
           ptx::tc_fence_after();
           if (tr && x == 0 && row == 0 && ai < 4) tr[490 + 4 * ai] = t4_clk();
-          ptx::mbar_wait(&l_full[x], ai & 1);
+          wait_epi(&l_full[x], ai & 1);
           l = l_sm[x][ai & 1][row];
           mr = m_sm[x][ai & 1][row];
           ptx::mbar_arrive(&l_free[x]);
