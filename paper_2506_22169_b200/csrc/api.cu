@@ -88,7 +88,7 @@ int64_t span_elems(int64_t batch, int64_t rows, int64_t cols, int64_t ld, int64_
 // Kernel-5 feature flags (Tc4Params::flags); MBCI_T5_FLAGS overrides (diagnostics).
 int t5_flags_default() {
   const char* e = getenv("MBCI_T5_FLAGS");
-  if (e) return atoi(e) & 0x1FFF;
+  if (e) return atoi(e) & 0xFFF;
   return 3857;  // bit 0: exp-phase turns; bit 2: spinning single-thread waits (A/B only);
                 // bits 4-5: hand the turn over that many 16-pair chunks before the end;
                 // bit 8: event-driven issuers (G1 / G2 in whichever order their inputs arrive);

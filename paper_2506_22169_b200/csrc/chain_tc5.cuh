@@ -100,48 +100,6 @@ __device__ __forceinline__ void t5_exp_row(uint32_t (&pk)[64], const uint32_t (&
   }
 }
 
-// Split-load variant (flags bit 12): the exponentials of chunks [C0, C1) of 16 column pairs of an
-// unmasked row (same arithmetic as t5_exp_row), the turn hand-over after chunk `arrive_after`.
-template <bool BF16, int EMU, int C0, int C1>
-__device__ __forceinline__ void t5_exp_chunks(uint32_t (&pk)[64], const uint32_t (&sr)[kT4BN], float sc, float m,
-                                              float2& l2a, float2& l2b, int arrive_after, uint32_t bar) {
-  const float2 sc2 = make_float2(sc, sc);
-  const float2 nm2 = make_float2(-m, -m);
-#pragma unroll
-  for (int ch = C0; ch < C1; ++ch) {
-#pragma unroll
-    for (int c = 0; c < 16; ++c) {
-      const int cp = ch * 16 + c;
-      const float2 z = __ffma2_rn(make_float2(__uint_as_float(sr[2 * cp]), __uint_as_float(sr[2 * cp + 1])), sc2, nm2);
-      float2 e;
-      if (EMU > 0 && ((cp * EMU) & 7) < EMU) {
-        e = t4_exp2_poly(z);
-      } else {
-        e.x = ptx::ex2(z.x);
-        e.y = ptx::ex2(z.y);
-      }
-      if (c & 1) l2b = __fadd2_rn(l2b, e); else l2a = __fadd2_rn(l2a, e);
-      pk[cp] = ptx::pack2<BF16>(e.x, e.y);
-    }
-    if (bar != 0 && ch == arrive_after) ptx::named_bar_arrive(bar, 64);
-  }
-}
-
-// packed 16-bit pairs [0, N) of pk scaled by a (the rare rescale of exponentials already taken)
-template <bool BF16, int N>
-__device__ __forceinline__ void t5_scale_packed(uint32_t (&pk)[64], float a) {
-#pragma unroll
-  for (int i = 0; i < N; ++i) {
-    float2 v;
-    if constexpr (BF16) {
-      v = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&pk[i]));
-    } else {
-      v = __half22float2(*reinterpret_cast<const __half2*>(&pk[i]));
-    }
-    pk[i] = ptx::pack2<BF16>(v.x * a, v.y * a);
-  }
-}
-
 // NONE / SCALE / RELU / GELU: the packed 16-bit row of op(s·S) into registers (the caller stores it
 // once G2 of the previous step has released P_x)
 template <bool BF16, bool ACT>
@@ -699,25 +657,13 @@ __global__ void __launch_bounds__(kT5Threads, 1)
         }
         const int valid = (p.causal ? min(n_lim, m_row + 1) : n_lim) - j * kT4BN;   // this thread's row
         const bool full = __all_sync(0xffffffffu, valid >= kT4BN);                   // warp-uniform
-        // flags bit 12 (softmax, unmasked rows): load columns 0-63, wait, then start the load of
-        // columns 64-127, which lands while the first half's exponentials run (one exposed
-        // 64-column TMEM load per step instead of a 128-column one); S_x is released after it
-        const bool split = (p.flags & 4096) && p.op == 2 && full && !(dbg & 1);
         uint32_t sr[kT4BN];
-        if (split) {
-          ptx::tmem_ld32(tS, &sr[0]);
-          ptx::tmem_ld32(tS + 32, &sr[32]);
-          ptx::tmem_wait_ld();
-          ptx::tmem_ld32(tS + 64, &sr[64]);
-          ptx::tmem_ld32(tS + 96, &sr[96]);
-        } else {
 #pragma unroll
-          for (int c = 0; c < kT4BN / 32; ++c) ptx::tmem_ld32(tS + c * 32, &sr[c * 32]);
-          ptx::tmem_wait_ld();
-          ptx::tc_fence_before();
-          __syncwarp();
-          if (lane0) ptx::mbar_arrive(&s_free[x]);   // S_x may be overwritten by G1(x, g + 1)
-        }
+        for (int c = 0; c < kT4BN / 32; ++c) ptx::tmem_ld32(tS + c * 32, &sr[c * 32]);
+        ptx::tmem_wait_ld();
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane0) ptx::mbar_arrive(&s_free[x]);   // S_x may be overwritten by G1(x, g + 1)
         if (p.op != 2) {
           // NONE / SCALE: padded keys have S = 0 and zero V rows (TMA fill), no masking needed
           if (p.flags & 512) {   // convert first, then wait for G2_x(g - 1) to release P_x
@@ -731,90 +677,6 @@ __global__ void __launch_bounds__(kT5Threads, 1)
             ptx::tc_fence_after();
             t4_cvt_row<BF16>(tP, sr, sc, p.op);
           }
-        } else if (split) {
-          // max of the first half (scale >= 0 or < 0: the extreme that maximises sc·S)
-          float a[8];
-#pragma unroll
-          for (int q = 0; q < 8; ++q)
-            a[q] = sc >= 0.f ? fmaxf(__uint_as_float(sr[2 * q]), __uint_as_float(sr[2 * q + 1]))
-                             : fminf(__uint_as_float(sr[2 * q]), __uint_as_float(sr[2 * q + 1]));
-#pragma unroll
-          for (int c = 16; c < 64; c += 16)
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-              a[q] = sc >= 0.f ? t4_red<false>(a[q], __uint_as_float(sr[c + 2 * q]), __uint_as_float(sr[c + 2 * q + 1]))
-                               : t4_red<true>(a[q], __uint_as_float(sr[c + 2 * q]), __uint_as_float(sr[c + 2 * q + 1]));
-          float mx = a[0];
-#pragma unroll
-          for (int q = 1; q < 8; ++q) mx = sc >= 0.f ? fmaxf(mx, a[q]) : fminf(mx, a[q]);
-          const float m_a = mx * sc;
-          bool p_ready = g == 0;
-          // lazy rescale of O_x / l (warp-uniform), as the one-pass path
-          auto rescale = [&](float m_new_lane, int halves_done) {
-            if (!p_ready) {
-              if (!(dbg & 128)) wait_sm(&p_free[x], ph ^ 1u);
-              ptx::tc_fence_after();
-              p_ready = true;
-            }
-            const float m_new = fmaxf(m_run, m_new_lane);
-            const float alpha = ptx::ex2(m_run - m_new);
-            l2.x *= alpha;
-            l2.y *= alpha;
-            l2b.x *= alpha;
-            l2b.y *= alpha;
-            m_run = m_new;
-            for (int c0 = 0; c0 < p.TL; c0 += 16) {
-              uint32_t r[16];
-              ptx::tmem_ld16(tO + c0, r);
-              ptx::tmem_wait_ld();
-#pragma unroll
-              for (int k = 0; k < 16; ++k) r[k] = __float_as_uint(__uint_as_float(r[k]) * alpha);
-              ptx::tmem_st16(tO + c0, r);
-            }
-            return alpha;
-          };
-          if (j == 0) {
-            m_run = m_a;
-          } else if (__any_sync(0xffffffffu, m_a > m_run + kT4Tau)) {
-            rescale(m_a, 0);   // waits for the second half's load too (tcgen05.wait::ld)
-          }
-          if (tr && row == 0 && g < kT4TrTiles) tr[T4TR(g, 2 + x)] = t4_clk_after(__float_as_uint(mx));
-          if (turns && (x == 1 || g > 0)) ptx::named_bar_sync(bar_mine, 64);
-          if (tr && row == 0 && g < kT4TrTiles) tr[T4TR(g, 4 + x)] = t4_clk();   // exps start
-          uint32_t pk[64];
-          t5_exp_chunks<BF16, EMU, 0, 2>(pk, sr, sc, m_run, l2, l2b, turn_chunk, turns ? bar_other : 0u);
-          // second half: landed during the exponentials above; S_x is free now
-          ptx::tmem_wait_ld();
-#pragma unroll
-          for (int c = 64; c < kT4BN; ++c) asm volatile("" : "+r"(sr[c]));   // uses stay after the wait
-          ptx::tc_fence_before();
-          __syncwarp();
-          if (lane0) ptx::mbar_arrive(&s_free[x]);
-#pragma unroll
-          for (int q = 0; q < 8; ++q)
-            a[q] = sc >= 0.f ? fmaxf(__uint_as_float(sr[64 + 2 * q]), __uint_as_float(sr[64 + 2 * q + 1]))
-                             : fminf(__uint_as_float(sr[64 + 2 * q]), __uint_as_float(sr[64 + 2 * q + 1]));
-#pragma unroll
-          for (int c = 80; c < kT4BN; c += 16)
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-              a[q] = sc >= 0.f ? t4_red<false>(a[q], __uint_as_float(sr[c + 2 * q]), __uint_as_float(sr[c + 2 * q + 1]))
-                               : t4_red<true>(a[q], __uint_as_float(sr[c + 2 * q]), __uint_as_float(sr[c + 2 * q + 1]));
-          mx = a[0];
-#pragma unroll
-          for (int q = 1; q < 8; ++q) mx = sc >= 0.f ? fmaxf(mx, a[q]) : fminf(mx, a[q]);
-          const float m_b = mx * sc;
-          if (__any_sync(0xffffffffu, m_b > m_run + kT4Tau)) {
-            const float alpha = rescale(m_b, 1);
-            t5_scale_packed<BF16, 32>(pk, alpha);   // the first half's p were taken against the old max
-          }
-          t5_exp_chunks<BF16, EMU, 2, 4>(pk, sr, sc, m_run, l2, l2b, turn_chunk, turns ? bar_other : 0u);
-          if (tr && row == 0 && g < kT4TrTiles) tr[T4TR(g, 6 + x)] = t4_clk();   // exps done
-          if (!p_ready) {
-            if (!(dbg & 128)) wait_sm(&p_free[x], ph ^ 1u);
-            ptx::tc_fence_after();
-          }
-          t5_store_p(tP, pk);
         } else {
           float mx;
           if (full)
