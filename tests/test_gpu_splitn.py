@@ -184,3 +184,20 @@ def test_split_errors(mbci):
     with pytest.raises(mbci.MbciError):
         ch.run_partial(x, x, x, x, None, None, 0)   # SOFTMAX without lse: INVALID
     ch.close()
+
+
+def test_merge_kernel_many_parts(mbci):
+    """More parts than the vector path's register budget (R > 8): the scalar path takes them."""
+    rng = np.random.default_rng(7)
+    R, b, M, L = 11, 2, 33, 64
+    parts = rng.standard_normal((R, b, M, L))
+    lse = rng.standard_normal((R, b, M)) * 3
+    lse[rng.random((R, b, M)) < 0.3] = -np.inf
+    Pt = torch.from_numpy(parts).to(torch.float16).cuda()
+    Lt = torch.from_numpy(lse).float().cuda()
+    E = torch.full((b, M, L), float("nan"), dtype=torch.float16, device="cuda")
+    mbci.merge_partials(Pt, Lt, E, "softmax")
+    torch.cuda.synchronize()
+    ref = lse_combine(Pt.double().cpu().numpy(), Lt.double().cpu().numpy())
+    got = E.double().cpu().numpy()
+    assert np.max(np.abs(got - ref) / (np.abs(ref) + 1.0)) <= 2e-3
