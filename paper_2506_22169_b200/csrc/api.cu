@@ -88,14 +88,16 @@ int64_t span_elems(int64_t batch, int64_t rows, int64_t cols, int64_t ld, int64_
 // Kernel-5 feature flags (Tc4Params::flags); MBCI_T5_FLAGS overrides (diagnostics).
 int t5_flags_default() {
   const char* e = getenv("MBCI_T5_FLAGS");
-  if (e) return atoi(e) & 0xFFF;
-  return 3857;  // bit 0: exp-phase turns; bit 2: spinning single-thread waits (A/B only);
+  if (e) return atoi(e) & 0x1FFF;
+  return 7953;  // bit 0: exp-phase turns; bit 2: spinning single-thread waits (A/B only);
                 // bits 4-5: hand the turn over that many 16-pair chunks before the end;
                 // bit 8: event-driven issuers (G1 / G2 in whichever order their inputs arrive);
                 // bit 9: linear ops convert S before waiting for P_x to be released
                 // (C4 K = L = 16: 49.0 -> 44.4 us; softmax configs within noise, round 2);
                 // bit 10: the epilogue sleeps between polls of its long O waits (~1 %);
-                // bit 11: softmax warps poll s_full / p_free with test_wait on SOFTMAX (~1 %)
+                // bit 11: softmax warps poll s_full / p_free with test_wait on SOFTMAX (~1 %);
+                // bit 12: P_x released first, each 16-column chunk of P stored as computed
+                // (16 packed registers live instead of 64: C6 -2 %, C2 within noise)
 }
 
 // Kernel-4 feature flags (MBCI_T4_FLAGS overrides): bit 10 the epilogue sleeps between polls.

@@ -42,10 +42,12 @@
 // written by one TMA bulk tensor store per 128-row tile (per-thread 16-B global stores from
 // the epilogue warps stretched the softmax warps' MUFU phases ~2x on the shared MIO queue).
 //
-// P_x hand-off: the softmax computes a step's exponentials into registers and waits for G2 of the
-// previous step (p_free) only before writing P_x, so the exp phase overlaps that G2 and its
-// issue latency (the wait-first order put P stored -> issuer wake -> G2 -> p_free on every
-// step's critical path).  A lazy rescale of O_x still waits first.
+// P_x hand-off: with the event-driven issuers (flags bit 8) G2 of the previous step has long
+// released P_x when a step's exponentials start, so (flags bit 12, the default) the softmax waits
+// for p_free first and stores each 16-column chunk of P as soon as it is computed (16 packed
+// registers live instead of 64).  Without bit 12 the exponentials go to registers and the wait
+// comes only before P is written (the order that paid with the in-order issuers).  A lazy rescale
+// of O_x waits first either way.
 //
 // Programmatic dependent launch: every CTA lets the next grid of the stream be scheduled at
 // once (griddepcontrol.launch_dependents) and waits for its prerequisite grids before its
@@ -119,6 +121,39 @@ template <bool BF16>
 __device__ __forceinline__ void t5_cvt_row(uint32_t (&pk)[64], const uint32_t (&sr)[kT4BN], float sc, int op) {
   if (op >= 3) t5_cvt_row_impl<BF16, true>(pk, sr, sc, op);   // one uniform branch per tile
   else t5_cvt_row_impl<BF16, false>(pk, sr, sc, op);
+}
+
+// As t5_exp_row, but each chunk's 16 packed P words go to TMEM (P_x, already released by G2 of the
+// previous step) as soon as they are computed: 16 packed registers live instead of 64 (flags bit 12)
+template <bool BF16, int EMU, bool MASKED>
+__device__ __forceinline__ void t5_exp_row_st(uint32_t tP, const uint32_t (&sr)[kT4BN], float sc, float m, int valid,
+                                              float2& l2a, float2& l2b, int arrive_after, uint32_t bar) {
+  const float2 sc2 = make_float2(sc, sc);
+  const float2 nm2 = make_float2(-m, -m);
+#pragma unroll
+  for (int ch = 0; ch < 4; ++ch) {
+    uint32_t pk[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+      const int cp = ch * 16 + c;
+      const float2 z = __ffma2_rn(make_float2(__uint_as_float(sr[2 * cp]), __uint_as_float(sr[2 * cp + 1])), sc2, nm2);
+      float2 e;
+      if (EMU > 0 && ((cp * EMU) & 7) < EMU) {
+        e = t4_exp2_poly(z);
+      } else {
+        e.x = ptx::ex2(z.x);
+        e.y = ptx::ex2(z.y);
+      }
+      if (MASKED) {
+        e.x = (2 * cp < valid) ? e.x : 0.f;
+        e.y = (2 * cp + 1 < valid) ? e.y : 0.f;
+      }
+      if (c & 1) l2b = __fadd2_rn(l2b, e); else l2a = __fadd2_rn(l2a, e);
+      pk[c] = ptx::pack2<BF16>(e.x, e.y);
+    }
+    ptx::tmem_st16(tP + ch * 16, pk);
+    if (bar != 0 && ch == arrive_after) ptx::named_bar_arrive(bar, 64);
+  }
 }
 
 // P_x <- the packed row (64 columns of 16-bit pairs), 16 columns per tcgen05.st
@@ -722,6 +757,18 @@ __global__ void __launch_bounds__(kT5Threads, 1)
           if (turns && (x == 1 || g > 0)) ptx::named_bar_sync(bar_mine, 64);
           if (tr && row == 0 && g < kT4TrTiles) tr[T4TR(g, 4 + x)] = t4_clk();   // exps start
           // the other slot's warp may start its turn after chunk turn_chunk of this one's
+          if (p.flags & 4096) {   // bit 12: P_x released first, each chunk stored as computed
+            if (!p_ready) {
+              if (!(dbg & 128)) wait_sm(&p_free[x], ph ^ 1u);
+              ptx::tc_fence_after();
+              p_ready = true;
+            }
+            if (full)
+              t5_exp_row_st<BF16, EMU, false>(tP, sr, sc, m_run, valid, l2, l2b, turn_chunk, turns ? bar_other : 0u);
+            else
+              t5_exp_row_st<BF16, 0, true>(tP, sr, sc, m_run, valid, l2, l2b, turn_chunk, turns ? bar_other : 0u);
+            if (tr && row == 0 && g < kT4TrTiles) tr[T4TR(g, 6 + x)] = t4_clk();   // exps done
+          } else {
           uint32_t pk[64];
           if (full)
             t5_exp_row<BF16, EMU, false>(pk, sr, sc, m_run, valid, l2, l2b, turn_chunk, turns ? bar_other : 0u);
@@ -733,6 +780,7 @@ __global__ void __launch_bounds__(kT5Threads, 1)
             ptx::tc_fence_after();
           }
           t5_store_p(tP, pk);
+          }
         }
         ptx::tmem_wait_st();
         if (tr && row == 0 && g < kT4TrTiles) tr[T4TR(g, 8 + x)] = t4_clk();
