@@ -242,7 +242,7 @@ __device__ __forceinline__ void t4_exp_row(uint32_t tS, const uint32_t (&sr)[kT4
 // NONE / SCALE: P = cvt(scale * S) for the 128 scores of the row, written as 16-bit P into TMEM
 // columns [0, 64) of the S buffer (no max, no exponentials, no row sum).
 // RELU / GELU (op 3 / 4): P = cvt(act(scale * S)).
-template <bool BF16, bool ACT>
+template <bool BF16, bool ACT, bool SCALED = true>
 __device__ __forceinline__ void t4_cvt_row_impl(uint32_t tS, const uint32_t (&sr)[kT4BN], float sc, int op) {
   const float2 sc2 = make_float2(sc, sc);
 #pragma unroll
@@ -251,7 +251,8 @@ __device__ __forceinline__ void t4_cvt_row_impl(uint32_t tS, const uint32_t (&sr
 #pragma unroll
     for (int c = 0; c < 16; ++c) {
       const int cp = ch * 16 + c;
-      float2 z = __fmul2_rn(make_float2(__uint_as_float(sr[2 * cp]), __uint_as_float(sr[2 * cp + 1])), sc2);
+      float2 z = make_float2(__uint_as_float(sr[2 * cp]), __uint_as_float(sr[2 * cp + 1]));
+      if (SCALED) z = __fmul2_rn(z, sc2);   // NONE (scale 1): P = cvt(S), no multiply
       if constexpr (ACT) {
         z.x = ptx::act(op, z.x);
         z.y = ptx::act(op, z.y);
@@ -264,6 +265,7 @@ __device__ __forceinline__ void t4_cvt_row_impl(uint32_t tS, const uint32_t (&sr
 template <bool BF16>
 __device__ __forceinline__ void t4_cvt_row(uint32_t tS, const uint32_t (&sr)[kT4BN], float sc, int op) {
   if (op >= 3) t4_cvt_row_impl<BF16, true>(tS, sr, sc, op);   // one uniform branch per tile
+  else if (op == 0) t4_cvt_row_impl<BF16, false, false>(tS, sr, sc, op);
   else t4_cvt_row_impl<BF16, false>(tS, sr, sc, op);
 }
 

@@ -104,12 +104,13 @@ __device__ __forceinline__ void t5_exp_row(uint32_t (&pk)[64], const uint32_t (&
 
 // NONE / SCALE / RELU / GELU: the packed 16-bit row of op(s·S) into registers (the caller stores it
 // once G2 of the previous step has released P_x)
-template <bool BF16, bool ACT>
+template <bool BF16, bool ACT, bool SCALED = true>
 __device__ __forceinline__ void t5_cvt_row_impl(uint32_t (&pk)[64], const uint32_t (&sr)[kT4BN], float sc, int op) {
   const float2 sc2 = make_float2(sc, sc);
 #pragma unroll
   for (int cp = 0; cp < 64; ++cp) {
-    float2 z = __fmul2_rn(make_float2(__uint_as_float(sr[2 * cp]), __uint_as_float(sr[2 * cp + 1])), sc2);
+    float2 z = make_float2(__uint_as_float(sr[2 * cp]), __uint_as_float(sr[2 * cp + 1]));
+    if constexpr (SCALED) z = __fmul2_rn(z, sc2);   // NONE (scale 1): P = cvt(S), no multiply
     if constexpr (ACT) {
       z.x = ptx::act(op, z.x);
       z.y = ptx::act(op, z.y);
@@ -120,6 +121,7 @@ __device__ __forceinline__ void t5_cvt_row_impl(uint32_t (&pk)[64], const uint32
 template <bool BF16>
 __device__ __forceinline__ void t5_cvt_row(uint32_t (&pk)[64], const uint32_t (&sr)[kT4BN], float sc, int op) {
   if (op >= 3) t5_cvt_row_impl<BF16, true>(pk, sr, sc, op);   // one uniform branch per tile
+  else if (op == 0) t5_cvt_row_impl<BF16, false, false>(pk, sr, sc, op);
   else t5_cvt_row_impl<BF16, false>(pk, sr, sc, op);
 }
 
