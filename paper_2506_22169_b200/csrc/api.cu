@@ -287,7 +287,9 @@ mbci_status_t setup_plan(mbci_chain* h) {
     h->tc4 = nullptr;
     h->tc5 = nullptr;
     if (p.kernel == 5)
-      h->tc5 = pick_tc5(d.dtype == MBCI_BF16, h->kch, d.b_layout, t4_emu_default());
+      // the linear ops run their own instantiation (EMU = -1), softmax the EMU variant
+      h->tc5 = pick_tc5(d.dtype == MBCI_BF16, h->kch, d.b_layout,
+                        d.op == MBCI_OP_SOFTMAX ? t4_emu_default() : -1);
     else if (p.kernel == 6)
       h->tc5 = pick_tc6(d.dtype == MBCI_BF16, h->kch, d.b_layout, t4_emu_default());
     else

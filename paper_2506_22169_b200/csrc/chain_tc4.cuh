@@ -251,8 +251,11 @@ __device__ __forceinline__ void t4_cvt_row_impl(uint32_t tS, const uint32_t (&sr
 #pragma unroll
     for (int c = 0; c < 16; ++c) {
       const int cp = ch * 16 + c;
-      float2 z = make_float2(__uint_as_float(sr[2 * cp]), __uint_as_float(sr[2 * cp + 1]));
-      if (SCALED) z = __fmul2_rn(z, sc2);   // NONE (scale 1): P = cvt(S), no multiply
+      float2 z;
+      if constexpr (SCALED)
+        z = __fmul2_rn(make_float2(__uint_as_float(sr[2 * cp]), __uint_as_float(sr[2 * cp + 1])), sc2);
+      else   // NONE (scale 1): P = cvt(S), no multiply
+        z = make_float2(__uint_as_float(sr[2 * cp]), __uint_as_float(sr[2 * cp + 1]));
       if constexpr (ACT) {
         z.x = ptx::act(op, z.x);
         z.y = ptx::act(op, z.y);
@@ -262,10 +265,12 @@ __device__ __forceinline__ void t4_cvt_row_impl(uint32_t tS, const uint32_t (&sr
     ptx::tmem_st16(tS + ch * 16, pk);
   }
 }
-template <bool BF16>
+// NOMUL_NONE: NONE converts S without its scale-1 multiply (kernel 5's linear instantiation; the
+// kernels that also carry the softmax path keep the code they were tuned with, see chain_tc5.cuh)
+template <bool BF16, bool NOMUL_NONE = false>
 __device__ __forceinline__ void t4_cvt_row(uint32_t tS, const uint32_t (&sr)[kT4BN], float sc, int op) {
   if (op >= 3) t4_cvt_row_impl<BF16, true>(tS, sr, sc, op);   // one uniform branch per tile
-  else if (op == 0) t4_cvt_row_impl<BF16, false, false>(tS, sr, sc, op);
+  else if (NOMUL_NONE && op == 0) t4_cvt_row_impl<BF16, false, false>(tS, sr, sc, op);
   else t4_cvt_row_impl<BF16, false>(tS, sr, sc, op);
 }
 

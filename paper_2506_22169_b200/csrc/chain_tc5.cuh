@@ -109,8 +109,11 @@ __device__ __forceinline__ void t5_cvt_row_impl(uint32_t (&pk)[64], const uint32
   const float2 sc2 = make_float2(sc, sc);
 #pragma unroll
   for (int cp = 0; cp < 64; ++cp) {
-    float2 z = make_float2(__uint_as_float(sr[2 * cp]), __uint_as_float(sr[2 * cp + 1]));
-    if constexpr (SCALED) z = __fmul2_rn(z, sc2);   // NONE (scale 1): P = cvt(S), no multiply
+    float2 z;
+    if constexpr (SCALED)
+      z = __fmul2_rn(make_float2(__uint_as_float(sr[2 * cp]), __uint_as_float(sr[2 * cp + 1])), sc2);
+    else   // NONE (scale 1): P = cvt(S), no multiply
+      z = make_float2(__uint_as_float(sr[2 * cp]), __uint_as_float(sr[2 * cp + 1]));
     if constexpr (ACT) {
       z.x = ptx::act(op, z.x);
       z.y = ptx::act(op, z.y);
@@ -118,10 +121,10 @@ __device__ __forceinline__ void t5_cvt_row_impl(uint32_t (&pk)[64], const uint32
     pk[cp] = ptx::pack2<BF16>(z.x, z.y);
   }
 }
-template <bool BF16>
+template <bool BF16, bool NOMUL_NONE>
 __device__ __forceinline__ void t5_cvt_row(uint32_t (&pk)[64], const uint32_t (&sr)[kT4BN], float sc, int op) {
   if (op >= 3) t5_cvt_row_impl<BF16, true>(pk, sr, sc, op);   // one uniform branch per tile
-  else if (op == 0) t5_cvt_row_impl<BF16, false, false>(pk, sr, sc, op);
+  else if (NOMUL_NONE && op == 0) t5_cvt_row_impl<BF16, false, false>(pk, sr, sc, op);
   else t5_cvt_row_impl<BF16, false>(pk, sr, sc, op);
 }
 
@@ -230,6 +233,13 @@ __global__ void __launch_bounds__(kT5Threads, 1)
   uint64_t* kv_empty = kv_full + S; // [S] the G2s reading the entry completed (two commits)
 
   const int warp = threadIdx.x >> 5;
+  // The linear ops NONE / SCALE / RELU / GELU run their own instantiation (EMU < 0), which carries
+  // only the linear path (no scale-1 multiply for NONE).  The softmax instantiations (EMU >= 0) keep
+  // the code they were tuned with: code placement alone moved C2 from 17.4 to 18.1-18.6 us when the
+  // linear path changed or was compiled out of them (profiles/r2_k5_layout_ab.txt)
+  constexpr bool kLinear = EMU < 0;
+  const int lin_op = p.op == 2 ? 0 : p.op;
+#define MBCI_T5_OP (kLinear ? lin_op : p.op)
   // Work-skipping diagnostics (MBCI_T4_DEBUG, trace build only; results are wrong by design):
   // 1 softmax and 16 epilogue keep only their barrier protocol, 2 / 4 the issuers skip the G2 / G1
   // MMAs (commits stay), 64 "TMA only": the issuers release each ring entry as soon as it lands
@@ -608,7 +618,7 @@ __global__ void __launch_bounds__(kT5Threads, 1)
         }
         ptx::tc_fence_after();
         float w0 = 1.f, w1 = 1.f, inv = 1.f;   // NONE / SCALE: E = O_0 + O_1
-        if (p.op == 2) {
+        if (MBCI_T5_OP == 2) {
           const float mstar = fmaxf(l[0] > 0.f ? m[0] : -INFINITY, l[1] > 0.f ? m[1] : -INFINITY);
           w0 = l[0] > 0.f ? ptx::ex2(m[0] - mstar) : 0.f;
           w1 = l[1] > 0.f ? ptx::ex2(m[1] - mstar) : 0.f;
@@ -659,10 +669,10 @@ __global__ void __launch_bounds__(kT5Threads, 1)
     const float sc = p.scale;
     // Exp-phase turns (flags bit 0, softmax only): named barriers 1-4 = slot 0's turn on SMSP q,
     // 5-8 = slot 1's; slot 0 goes first.
-    const bool turns = (p.flags & 1) != 0 && p.op == 2;
+    const bool turns = (p.flags & 1) != 0 && MBCI_T5_OP == 2;
     // flags bit 11: on SOFTMAX the softmax warps poll s_full / p_free with test_wait instead of
     // try_wait (C2 -1.3 %; on the linear ops polling costs 7 %, so they keep try_wait)
-    const bool sm_spin = (p.flags & 2048) != 0 && p.op == 2;
+    const bool sm_spin = (p.flags & 2048) != 0 && MBCI_T5_OP == 2;
     auto wait_sm = [&](uint64_t* bar, uint32_t parity) {
       if (sm_spin) ptx::mbar_spin(bar, parity); else ptx::mbar_wait(bar, parity);
     };
@@ -701,18 +711,18 @@ __global__ void __launch_bounds__(kT5Threads, 1)
         ptx::tc_fence_before();
         __syncwarp();
         if (lane0) ptx::mbar_arrive(&s_free[x]);   // S_x may be overwritten by G1(x, g + 1)
-        if (p.op != 2) {
+        if (MBCI_T5_OP != 2) {
           // NONE / SCALE: padded keys have S = 0 and zero V rows (TMA fill), no masking needed
           if (p.flags & 512) {   // convert first, then wait for G2_x(g - 1) to release P_x
             uint32_t pk[64];
-            t5_cvt_row<BF16>(pk, sr, sc, p.op);
+            t5_cvt_row<BF16, kLinear>(pk, sr, sc, MBCI_T5_OP);
             if (g > 0) wait_sm(&p_free[x], ph ^ 1u);
             ptx::tc_fence_after();
             t5_store_p(tP, pk);
           } else {
             if (g > 0) wait_sm(&p_free[x], ph ^ 1u);   // G2_x(g - 1) has read P_x
             ptx::tc_fence_after();
-            t4_cvt_row<BF16>(tP, sr, sc, p.op);
+            t4_cvt_row<BF16, kLinear>(tP, sr, sc, MBCI_T5_OP);
           }
         } else {
           float mx;
@@ -793,7 +803,7 @@ __global__ void __launch_bounds__(kT5Threads, 1)
       // l_full's parity protocol allows one phase in flight: publishing l of item ai waits
       // until the epilogue has read item ai - 1's.
       if (ai >= 1) ptx::mbar_wait(&l_free[x], (ai - 1) & 1);
-      l_sm[x][ai & 1][row] = p.op == 2 ? (l2.x + l2.y) + (l2b.x + l2b.y) : 1.0f;   // E = O / l
+      l_sm[x][ai & 1][row] = MBCI_T5_OP == 2 ? (l2.x + l2.y) + (l2b.x + l2b.y) : 1.0f;   // E = O / l
       m_sm[x][ai & 1][row] = m_run;
       __syncwarp();
       if (lane0) ptx::mbar_arrive(&l_full[x]);
@@ -810,5 +820,6 @@ __global__ void __launch_bounds__(kT5Threads, 1)
     ptx::tmem_dealloc(tmem, 512);
   }
 }
+#undef MBCI_T5_OP
 
 }  // namespace mbci

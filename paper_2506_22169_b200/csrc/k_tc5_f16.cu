@@ -8,6 +8,7 @@ constexpr bool kBF16 = false;
 template <int KCH, int BL>
 Tc5Kernel pick_emu(int emu) {
   switch (emu) {
+    case -1: return (Tc5Kernel)k_chain_tc5<kBF16, KCH, BL, -1>;   // linear ops
     case 0: return (Tc5Kernel)k_chain_tc5<kBF16, KCH, BL, 0>;
     case 2: return (Tc5Kernel)k_chain_tc5<kBF16, KCH, BL, 2>;
     case 4: return (Tc5Kernel)k_chain_tc5<kBF16, KCH, BL, 4>;
