@@ -126,20 +126,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
   if (mbar_try_wait(addr, parity)) return;
   const uint64_t t0 = globaltimer();
-#if MBCI_WAIT2
-  // A/B build: the time check in its own loop level, the poll loop kept rolled
-  for (;;) {
-#pragma unroll 1
-    for (uint32_t i = 0; i < 1024u; ++i)
-      if (mbar_try_wait(addr, parity)) return;
-    if (globaltimer() - t0 > 4000000000ull) __trap();
-  }
-#else
   uint32_t spins = 0;
   while (!mbar_try_wait(addr, parity)) {
     if (((++spins) & 1023u) == 0 && globaltimer() - t0 > 4000000000ull) __trap();
   }
-#endif
 }
 // Long waits of latency-tolerant roles (the epilogue waits a whole item for O): try_wait, then
 // sleep with exponential backoff up to cap_ns between polls, so the waiting warp leaves its
